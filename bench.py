@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""Benchmark of the Köhler contrast-curve hot path on B200.
+
+Workload (BASELINE.json configs[1], "C2"): one 5184x3456 uint8 image
+(gradient + 40 ellipses + N(0,5^2), seeded), full N4 curve (u64 sum/count),
+IEEE f64 mean curve, optimal threshold and top-6 local maxima.  One step =
+one pass of that pipeline over the image.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1: one fused launch per step (K1 accumulate + K3 reconstruct + K4 select).
+N > 1 (torchrun, one process per GPU, NCCL): the image is split into row
+bands with a one-row halo (proj/src/fast.cpp:42-57); per step each rank runs
+K1 on its band, one all-reduce of the 512 u64 partials, then K4 — strong
+scaling (the image is fixed).  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.  L2 (126 MB) is defeated
+by rotating through input copies totalling > 2x L2.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libkohler_ref.so, compiled from the reference sources) on this
+host's cores with the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+METRIC = "Gpixel/s (full 8-bit N4 Koehler curve + optimal threshold + top-6 maxima)"
+UNIT = "Gpixel/s"
+K_TOP = 6
+CONFIG_NAME = "C2"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    --set full capture summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(CONFIG_NAME)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the workload runs."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_input(device="cpu"):
+    from paper_1707_05062_b200 import synth
+    return synth.generate(CONFIG_NAME, device=device)[0]
+
+
+def cpu_reference_time(img: np.ndarray, budget_s: float, max_runs: int):
+    """Median steady_clock time of the reference pipeline (curve + mean +
+    t0 + top-6) with workers = all host cores — bench.cpp:171-185 method."""
+    import oracle
+    ref = oracle.Reference()
+    cores = os.cpu_count() or 1
+    with ref.image(img) as im:
+        one = ref.lib.kref_time_pipeline(im.h, cores, K_TOP, 1, 1)
+        runs = int(max(3, min(max_runs, budget_s / max(one, 1e-6))))
+        med = ref.lib.kref_time_pipeline(im.h, cores, K_TOP, 0, runs)
+    return med, runs, cores, ref.active_kernel()
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the reference's CPU implementation on this host."""
+    if rank != 0:
+        return
+    import oracle
+    img = make_input("cpu").numpy()
+    h, w = img.shape
+    ref = oracle.Reference()
+    cores = os.cpu_count() or 1
+    with ref.image(img) as im:
+        for _ in range(args.warmup):
+            ref.lib.kref_time_pipeline(im.h, cores, K_TOP, 0, 1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ref.lib.kref_time_pipeline(im.h, cores, K_TOP, 0, 1)
+        el = time.perf_counter() - t0
+    val = w * h * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"{CONFIG_NAME} {w}x{h} gradient+ellipses+N(0,5^2), k={K_TOP}",
+                   "parallelism": f"{cores} host threads (reference fast_contrast_curve workers)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"full {CONFIG_NAME} image per step, kernel={ref.active_kernel()}"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-budget", type=float, default=12.0,
+                    help="seconds of CPU-baseline sampling (rank 0, N=1)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: min(steps, 200)")
+    ap.add_argument("--graph", action="store_true", help="replay steps from CUDA graphs")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_1707_05062_b200 import Context
+    from paper_1707_05062_b200.bands import BandedAnalyzer
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ctx = Context(dev.index)
+    img = make_input("cpu")
+    h, w = img.shape
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        pitch = (w + 127) // 128 * 128
+        img_bytes = pitch * h
+        copies = max(2, (2 * l2) // img_bytes + 1)
+        buf = torch.zeros((copies, h, pitch), dtype=torch.uint8, device=dev)
+        buf[:, :, :w] = img.to(dev)[None]
+        out = {"sums": torch.zeros(256, dtype=torch.int64, device=dev),
+               "cards": torch.zeros(256, dtype=torch.int64, device=dev),
+               "values": torch.zeros(256, dtype=torch.float64, device=dev),
+               "defined": torch.zeros(256, dtype=torch.uint8, device=dev),
+               "t0": torch.zeros(1, dtype=torch.int32, device=dev),
+               "topk": torch.zeros(K_TOP, dtype=torch.int32, device=dev),
+               "topk_count": torch.zeros(1, dtype=torch.int32, device=dev),
+               "status": torch.zeros(1, dtype=torch.int32, device=dev)}
+
+        def step(i):
+            ctx.analyze_batch_device(buf[i % copies], w, h, pitch, img_bytes, 1, K_TOP, out, stream)
+        launches_per_step = 1
+        bytes_per_step = w * h
+        parallel = "1 GPU, one fused launch per step"
+    else:
+        ba = BandedAnalyzer(ctx, w, h, world, rank, K_TOP)
+        pitch = (w + 127) // 128 * 128
+        rows = ba.rows_held
+        band_bytes = max(rows, 1) * pitch
+        copies = max(2, (2 * l2) // band_bytes + 1)
+        buf = torch.zeros((copies, max(rows, 1), pitch), dtype=torch.uint8, device=dev)
+        if rows:
+            buf[:, :rows, :w] = img[ba.lo:ba.hi].to(dev)[None]
+        out = ba.out
+
+        def step(i):
+            ba.step(buf[i % copies], pitch)
+        launches_per_step = 2
+        bytes_per_step = w * h  # whole job processes the full image per step
+        parallel = f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64, strong scaling"
+
+    # correctness gate before timing (bench.cpp:141-161 semantics)
+    step(0)
+    torch.cuda.synchronize()
+    if rank == 0:
+        import oracle
+        exp = oracle.Oracle().analyze(img.numpy(), K_TOP)
+        got_t0 = int(out["t0"][0])
+        got_tk = out["topk"][: int(out["topk_count"][0])].tolist()
+        ok = got_t0 == exp["t0"] and got_tk == exp["topk"]
+        if world == 1:
+            ok = ok and np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"]) \
+                and np.array_equal(out["cards"].cpu().numpy().view(np.uint64), exp["card"])
+        if not ok:
+            raise SystemExit("refusing to time: GPU result differs from the oracle")
+
+    for i in range(args.warmup):
+        step(i)
+    graphs = None
+    if args.graph:
+        graphs = []
+        for c in range(copies):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(c)
+            graphs.append(g)
+        for g in graphs:
+            g.replay()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(dev.index if world == 1 else local).start()
+    time.sleep(0.1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        if graphs:
+            graphs[i % copies].replay()
+        else:
+            step(i)
+    e1.record(stream)
+    e1.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = bytes_per_step * args.steps / (ms * 1e-3) / 1e9
+
+    # kernel-level timing of K1 alone (its own events, same stream), for the roofline
+    kern_ms = None
+    if world == 1:
+        kern_ms = ms_step  # one launch per step: the step IS the kernel
+    else:
+        k0 = torch.cuda.Event(enable_timing=True)
+        k1 = torch.cuda.Event(enable_timing=True)
+        nk = min(args.steps, 200)
+        k0.record(stream)
+        for i in range(nk):
+            if ba.r1 > ba.r0:
+                ctx.band_curve_device(buf[i % copies], w, pitch, h, ba.r0, ba.r1,
+                                      ba.curve.data_ptr(), ba.curve.data_ptr() + 2048, stream)
+        k1.record(stream)
+        k1.synchronize()
+        kern_ms = k0.elapsed_time(k1) / nk
+    peak, peak_src = peaks()
+    kbytes = w * h if world == 1 else (ba.r1 - ba.r0) * w
+    achieved = kbytes / (kern_ms * 1e-3) / 1e9
+
+    line = None
+    if rank == 0:
+        e2e = None
+        cpu = None
+        if world == 1:
+            e2e = measure_e2e(ctx, img, args)
+            med, runs, cores, kern = cpu_reference_time(img.numpy(), args.cpu_budget, 2000)
+            cpu = {"value": w * h / med / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"full {CONFIG_NAME} image, median of {runs} runs (1 warm-up), "
+                             f"workers={cores}, kernel={kern}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": f"{CONFIG_NAME} {w}x{h} gradient+40 ellipses+N(0,5^2), seed "
+                                   f"0x51C2, k={K_TOP}",
+                       "parallelism": parallel,
+                       "l2": f"rotating {copies} input copies ({copies * buf[0].numel() / 1e6:.0f} MB"
+                             f" > 2x L2 {l2 / 1e6:.0f} MB)",
+                       "launch": "cuda-graph replay" if graphs else "eager"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "wide_kernel<true> (K1+K3+K4 fused)" if world == 1
+                         else "wide_kernel<true> band partial (K1)",
+                         "algorithmic_bytes_per_launch": kbytes, "kernel_ms": kern_ms,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_e2e(ctx, img, args):
+    """Same metric through the public host API (kohler_cuda_analyze via
+    Context.analyze_batch): pinned host image -> H2D -> fused kernel -> D2H
+    of curve + mean curve + thresholds, every step, wall-clocked."""
+    import ctypes as C
+    h, w = img.shape
+    pinned = torch.empty((h, w), dtype=torch.uint8).pin_memory()
+    pinned.copy_(img)
+    n = args.e2e_steps or min(args.steps, 200)
+    res = {k: np.zeros(256, np.uint64) for k in ("s", "c")}
+    vals = np.zeros(256, np.float64)
+    dfn = np.zeros(256, np.uint8)
+    t0 = np.zeros(1, np.int32)
+    tk = np.zeros(K_TOP, np.int32)
+    cnt = np.zeros(1, np.int32)
+    lib = ctx._lib
+
+    def call():
+        return lib.kohler_cuda_analyze(ctx.handle, pinned.data_ptr(), w, h, w, K_TOP,
+                                       res["s"].ctypes.data, res["c"].ctypes.data,
+                                       vals.ctypes.data, dfn.ctypes.data, t0.ctypes.data,
+                                       tk.ctypes.data, cnt.ctypes.data)
+    for _ in range(3):
+        call()
+    st = time.perf_counter()
+    for _ in range(n):
+        rc = call()
+        if rc not in (0, 1):
+            raise RuntimeError("e2e call failed")
+    el = time.perf_counter() - st
+    d2h = 256 * 8 * 2 + 256 * 8 + 256 + 4 * 3 + 4 * K_TOP
+    return {"value": w * h * n / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": w * h,
+            "d2h_bytes_per_step": d2h, "steps": n,
+            "path": "kohler_cuda_analyze (host API), pinned input, wall clock"}
+
+
+if __name__ == "__main__":
+    main()

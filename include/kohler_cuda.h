@@ -1,0 +1,143 @@
+/*
+ * kohler_cuda.h — C ABI of the B200 (sm_100a) Köhler contrast-curve path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch
+ * types, status codes instead of exceptions.  The C++ drop-in
+ * (headers under include/kohler/, libkohler_b200.so) and the Python host layer
+ * (paper_1707_05062_b200/) sit on top of it; INTEGRATION.md shows the
+ * reference-side bindings.
+ *
+ * Reference interfaces replaced (files under /root/reference/proj):
+ *   kohler_cuda_curve            -> kohler::fast_contrast_curve
+ *                                   (include/kohler/contrast.hpp:18, src/fast.cpp:36-62)
+ *   kohler_cuda_band_curve_device-> the per-row-block partial of src/fast.cpp:18-32,53-57
+ *                                   (accumulate_rows); partials merge by entrywise u64
+ *                                   sum exactly like merge_accumulators (src/curve.cpp:16-30)
+ *   kohler_cuda_mean_contrast    -> kohler::mean_contrast (include/kohler/threshold.hpp:50,
+ *                                   src/threshold.cpp:9-23)
+ *   kohler_cuda_optimal_threshold-> kohler::optimal_threshold (threshold.hpp:54,
+ *                                   src/threshold.cpp:25-37)
+ *   kohler_cuda_top_k_local_maxima -> kohler::top_k_local_maxima (threshold.hpp:60,
+ *                                   src/threshold.cpp:39-82)
+ *   kohler_cuda_analyze[_batch]  -> the per-image pipeline curve -> mean_contrast ->
+ *                                   optimal_threshold -> top_k_local_maxima of
+ *                                   tools/kohler_main.cpp:91-107 and src/bench.cpp:263-277
+ *
+ * Results are bit-identical to the reference: integer curves exactly, the
+ * double curve bit-for-bit (IEEE division of exactly-representable operands),
+ * thresholds exactly.
+ *
+ * Threading: every call is reentrant; calls on one context are serialised by
+ * the context's mutex.  *_device calls are asynchronous on the given stream
+ * and use the context's workspace: issue them for one context from one
+ * stream (or order the streams yourself).
+ */
+#ifndef KOHLER_CUDA_H
+#define KOHLER_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KOHLER_LEVELS 256
+
+/* Status codes. */
+#define KOHLER_OK 0
+#define KOHLER_NO_BOUNDARY 1      /* reference: NoBoundaryError (threshold.hpp:14-20)  */
+#define KOHLER_INVALID_ARGUMENT 2 /* reference: std::invalid_argument                  */
+#define KOHLER_CUDA_ERROR 3       /* reference: none (runtime_error in the drop-in)     */
+#define KOHLER_OUT_OF_MEMORY 4
+
+typedef struct kohler_cuda_ctx kohler_cuda_ctx;
+
+/* Version of this ABI (major*100 + minor). */
+int kohler_cuda_abi_version(void);
+
+/* Message of the last failing call made by the calling thread ("" if none). */
+const char *kohler_cuda_last_error(void);
+
+/* Context bound to one CUDA device: owns a stream, device workspace and
+ * pinned staging.  device < 0 means the current device. */
+int kohler_cuda_create(int device, kohler_cuda_ctx **out);
+void kohler_cuda_destroy(kohler_cuda_ctx *ctx);
+int kohler_cuda_device(const kohler_cuda_ctx *ctx);
+
+/* ---- host-memory API (synchronous) ------------------------------------ */
+
+/* Curve of one w x h image with row pitch `pitch` (>= w) bytes in host
+ * memory.  sum/card: 256 u64 each.  Replaces fast_contrast_curve. */
+int kohler_cuda_curve(kohler_cuda_ctx *ctx, const uint8_t *px, int w, int h, size_t pitch,
+                      uint64_t *sum, uint64_t *card);
+
+/* Definition-level curve (one full scan of ordered 4-neighbour pairs per
+ * threshold) computed by a separate naive GPU kernel that shares no code with
+ * the accumulation path.  Replaces kohler::direct_contrast_curve
+ * (include/kohler/contrast.hpp:11, src/direct.cpp:10-43).  Θ(256·4·N): meant
+ * for checking, not for speed. */
+int kohler_cuda_direct_curve(kohler_cuda_ctx *ctx, const uint8_t *px, int w, int h, size_t pitch,
+                             uint64_t *sum, uint64_t *card);
+
+/* Full per-image pipeline on host buffers.  Any output pointer may be NULL.
+ * values: 256 doubles; defined: 256 bytes (0/1); topk: k ints, ascending;
+ * *topk_count = number written.  Returns KOHLER_NO_BOUNDARY (t0 = -1,
+ * count 0, curves still written) for a boundary-free image.  k >= 1. */
+int kohler_cuda_analyze(kohler_cuda_ctx *ctx, const uint8_t *px, int w, int h, size_t pitch,
+                        int k, uint64_t *sum, uint64_t *card, double *values,
+                        uint8_t *defined, int *t0, int *topk, int *topk_count);
+
+/* Batch of n images of identical size; image i starts at px + i*image_stride.
+ * Per-image outputs are laid out contiguously (256 per image for curves,
+ * k per image for topk).  status: n ints (KOHLER_OK / KOHLER_NO_BOUNDARY),
+ * may be NULL.  Returns KOHLER_OK unless an argument or CUDA error occurs. */
+int kohler_cuda_analyze_batch(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w, int h,
+                              size_t pitch, size_t image_stride, int k, uint64_t *sums,
+                              uint64_t *cards, double *values, uint8_t *defined, int *t0s,
+                              int *topks, int *topk_counts, int *status);
+
+/* Selection on host curves (run on the GPU).  n = number of levels
+ * (0..4096).  Replace mean_contrast / optimal_threshold / top_k_local_maxima. */
+int kohler_cuda_mean_contrast(kohler_cuda_ctx *ctx, const uint64_t *sum, const uint64_t *card,
+                              int n, double *values, uint8_t *defined);
+int kohler_cuda_optimal_threshold(kohler_cuda_ctx *ctx, const double *values,
+                                  const uint8_t *defined, int n, int *t0);
+int kohler_cuda_top_k_local_maxima(kohler_cuda_ctx *ctx, const double *values,
+                                   const uint8_t *defined, int n, int k, int *out, int *count);
+
+/* ---- device-memory API (asynchronous on `stream`, a cudaStream_t) ------ */
+
+/* Batched pipeline on device-resident images (the throughput path).  All
+ * pointers are device pointers; outputs as in kohler_cuda_analyze_batch and
+ * may be NULL.  Fast path when px, pitch and image_stride are 16-byte
+ * aligned; otherwise a byte-load path with identical results. */
+int kohler_cuda_analyze_batch_device(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w,
+                                     int h, size_t pitch, size_t image_stride, int k,
+                                     uint64_t *sums, uint64_t *cards, double *values,
+                                     uint8_t *defined, int *t0s, int *topks,
+                                     int *topk_counts, int *status, void *stream);
+
+/* Row-band partial curve (multi-GPU row decomposition).  `band` points at
+ * global row r0 of an image of h_total rows; it holds the band's own rows
+ * [r0, r1) plus, when r1 < h_total, the one-row halo r1.  The partial counts
+ * exactly the pairs rows [r0, r1) own (right pairs in each row, down pairs
+ * (i, i+1)), so partials of a partition of [0, h_total) sum (u64) to the
+ * whole-image curve.  sum/card: 256 u64 device outputs. */
+int kohler_cuda_band_curve_device(kohler_cuda_ctx *ctx, const uint8_t *band, int w,
+                                  size_t pitch, int h_total, int r0, int r1, uint64_t *sum,
+                                  uint64_t *card, void *stream);
+
+/* Selection on device curves: n_curves curves of `levels` entries each. */
+int kohler_cuda_select_device(kohler_cuda_ctx *ctx, const uint64_t *sums,
+                              const uint64_t *cards, int n_curves, int levels, int k,
+                              double *values, uint8_t *defined, int *t0s, int *topks,
+                              int *topk_counts, int *status, void *stream);
+
+/* Number of kernels the last call on this context launched (bench evidence). */
+int kohler_cuda_last_launch_count(const kohler_cuda_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KOHLER_CUDA_H */

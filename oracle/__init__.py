@@ -1,0 +1,291 @@
+"""Checkers for the Köhler path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline /
+``--impl reference`` legs may import this package, and only as the checker or
+the timed CPU baseline — never as part of the product path.
+
+* :class:`Oracle`    — ctypes over ``_build/libkohler_oracle.so``, the C
+  restatement in kohler_oracle.c (each function cites the reference lines it
+  follows).
+* :class:`Reference` — ctypes over ``_ref/libkohler_ref.so``, the reference
+  library itself compiled from /root/reference/proj/src by oracle/Makefile
+  (namespace-renamed, plus the C shim ref_shim.cpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libkohler_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libkohler_ref.so")
+REFERENCE_SRC = "/root/reference/proj"
+
+NO_BOUNDARY = 1
+INVALID_K = 2
+
+
+def build(ref: bool = True) -> None:
+    """Compile the C restatement and, when /root/reference is present, the
+    reference library (outputs only under oracle/_build and oracle/_ref)."""
+    targets = [ORACLE_SO]
+    if ref and os.path.isdir(REFERENCE_SRC):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Oracle:
+    """The C restatement of the reference algorithm (kohler_oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build(ref=False)
+        self.lib = C.CDLL(path)
+        vp, i = C.c_void_p, C.c_int
+        for name, args, res in [
+            ("oracle_pair_contribution", [i, i, vp, vp], None),
+            ("oracle_curve_rows", [vp, i, i, C.c_size_t, i, i, vp, vp], None),
+            ("oracle_fast_curve", [vp, i, i, vp, vp], None),
+            ("oracle_fast_curve_blocks", [vp, i, i, C.c_uint, vp, vp], None),
+            ("oracle_direct_curve", [vp, i, i, vp, vp], None),
+            ("oracle_mean_contrast", [vp, vp, i, vp, vp], None),
+            ("oracle_optimal_threshold", [vp, vp, i], i),
+            ("oracle_top_k_local_maxima", [vp, vp, i, i, vp, vp], i),
+            ("oracle_identities", [vp, i, i, vp, vp], None),
+            ("oracle_analyze", [vp, i, i, i, vp, vp, vp, vp, vp, vp, vp], i),
+        ]:
+            f = getattr(self.lib, name)
+            f.argtypes = args
+            f.restype = res
+
+    @staticmethod
+    def _img(px):
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        if px.ndim != 2:
+            raise ValueError("expected a 2-D image")
+        return px, px.shape[1], px.shape[0]
+
+    def pair_contribution(self, lo, hi):
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.oracle_pair_contribution(int(lo), int(hi), _p(s), _p(c))
+        return s, c
+
+    def fast_curve(self, px):
+        px, w, h = self._img(px)
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.oracle_fast_curve(_p(px), w, h, _p(s), _p(c))
+        return s, c
+
+    def curve_rows(self, px, r0, r1):
+        """Partial curve of the pairs rows [r0, r1) own (fast.cpp:18-32)."""
+        px, w, h = self._img(px)
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.oracle_curve_rows(_p(px), w, h, w, int(r0), int(r1), _p(s), _p(c))
+        return s, c
+
+    def fast_curve_blocks(self, px, blocks):
+        px, w, h = self._img(px)
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.oracle_fast_curve_blocks(_p(px), w, h, int(blocks), _p(s), _p(c))
+        return s, c
+
+    def direct_curve(self, px):
+        px, w, h = self._img(px)
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.oracle_direct_curve(_p(px), w, h, _p(s), _p(c))
+        return s, c
+
+    def mean_contrast(self, s, c):
+        s = np.ascontiguousarray(s, np.uint64)
+        c = np.ascontiguousarray(c, np.uint64)
+        n = s.shape[0]
+        v = np.zeros(n, np.float64)
+        d = np.zeros(n, np.uint8)
+        self.lib.oracle_mean_contrast(_p(s), _p(c), n, _p(v), _p(d))
+        return v, d
+
+    def optimal_threshold(self, v, d):
+        v = np.ascontiguousarray(v, np.float64)
+        d = np.ascontiguousarray(d, np.uint8)
+        return int(self.lib.oracle_optimal_threshold(_p(v), _p(d), v.shape[0]))
+
+    def top_k(self, v, d, k):
+        """-> (status, thresholds); status 0 ok, 1 no boundary, 2 invalid k."""
+        v = np.ascontiguousarray(v, np.float64)
+        d = np.ascontiguousarray(d, np.uint8)
+        out = np.zeros(max(int(k), 1), np.int32)
+        cnt = np.zeros(1, np.int32)
+        st = self.lib.oracle_top_k_local_maxima(_p(v), _p(d), v.shape[0], int(k), _p(out), _p(cnt))
+        return int(st), [int(t) for t in out[: cnt[0]]]
+
+    def identities(self, px):
+        px, w, h = self._img(px)
+        tv = np.zeros(1, np.uint64)
+        qs = np.zeros(1, np.uint64)
+        self.lib.oracle_identities(_p(px), w, h, _p(tv), _p(qs))
+        return int(tv[0]), int(qs[0])
+
+    def analyze(self, px, k=6):
+        """-> dict(sum, card, values, defined, t0, topk, status)."""
+        px, w, h = self._img(px)
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        v = np.zeros(256, np.float64)
+        d = np.zeros(256, np.uint8)
+        t0 = np.zeros(1, np.int32)
+        tk = np.zeros(k, np.int32)
+        cnt = np.zeros(1, np.int32)
+        st = self.lib.oracle_analyze(_p(px), w, h, int(k), _p(s), _p(c), _p(v), _p(d), _p(t0),
+                                     _p(tk), _p(cnt))
+        return dict(sum=s, card=c, values=v, defined=d, t0=int(t0[0]),
+                    topk=[int(t) for t in tk[: cnt[0]]], status=int(st))
+
+
+class Reference:
+    """The reference library compiled from /root/reference (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (needs /root/reference at build time)")
+        self.lib = C.CDLL(path)
+        vp, i, u = C.c_void_p, C.c_int, C.c_uint
+        for name, args, res in [
+            ("kref_active_kernel", [], C.c_char_p),
+            ("kref_image_new", [vp, i, i], vp),
+            ("kref_image_free", [vp], None),
+            ("kref_fast_curve", [vp, u, vp, vp], i),
+            ("kref_direct_curve", [vp, vp, vp], i),
+            ("kref_pair_contribution", [i, i, vp, vp], None),
+            ("kref_mean_contrast", [vp, vp, i, vp, vp], None),
+            ("kref_optimal_threshold", [vp, vp, i, vp], i),
+            ("kref_top_k", [vp, vp, i, i, vp, vp], i),
+            ("kref_pipeline", [vp, u, i, vp, vp, vp, vp, vp, vp, vp], i),
+            ("kref_pipeline_batch", [vp, i, u, i, i, vp, vp, vp, vp, vp], i),
+            ("kref_time_pipeline", [vp, u, i, i, i], C.c_double),
+        ]:
+            f = getattr(self.lib, name)
+            f.argtypes = args
+            f.restype = res
+
+    def active_kernel(self) -> str:
+        return self.lib.kref_active_kernel().decode()
+
+    def image(self, px) -> "RefImage":
+        return RefImage(self, px)
+
+    def fast_curve(self, px, workers=1):
+        with self.image(px) as im:
+            s = np.zeros(256, np.uint64)
+            c = np.zeros(256, np.uint64)
+            st = self.lib.kref_fast_curve(im.h, int(workers), _p(s), _p(c))
+            if st:
+                raise ValueError("fast_contrast_curve: workers must be at least 1")
+            return s, c
+
+    def direct_curve(self, px):
+        with self.image(px) as im:
+            s = np.zeros(256, np.uint64)
+            c = np.zeros(256, np.uint64)
+            self.lib.kref_direct_curve(im.h, _p(s), _p(c))
+            return s, c
+
+    def pair_contribution(self, lo, hi):
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        self.lib.kref_pair_contribution(int(lo), int(hi), _p(s), _p(c))
+        return s, c
+
+    def mean_contrast(self, s, c):
+        s = np.ascontiguousarray(s, np.uint64)
+        c = np.ascontiguousarray(c, np.uint64)
+        n = s.shape[0]
+        v = np.zeros(n, np.float64)
+        d = np.zeros(n, np.uint8)
+        self.lib.kref_mean_contrast(_p(s), _p(c), n, _p(v), _p(d))
+        return v, d
+
+    def optimal_threshold(self, v, d):
+        v = np.ascontiguousarray(v, np.float64)
+        d = np.ascontiguousarray(d, np.uint8)
+        t = np.zeros(1, np.int32)
+        st = self.lib.kref_optimal_threshold(_p(v), _p(d), v.shape[0], _p(t))
+        return -1 if st else int(t[0])
+
+    def top_k(self, v, d, k):
+        v = np.ascontiguousarray(v, np.float64)
+        d = np.ascontiguousarray(d, np.uint8)
+        out = np.zeros(max(int(k), 1) + v.shape[0], np.int32)
+        cnt = np.zeros(1, np.int32)
+        st = self.lib.kref_top_k(_p(v), _p(d), v.shape[0], int(k), _p(out), _p(cnt))
+        return int(st), [int(t) for t in out[: cnt[0]]]
+
+    def analyze(self, px, k=6, workers=1):
+        with self.image(px) as im:
+            s = np.zeros(256, np.uint64)
+            c = np.zeros(256, np.uint64)
+            v = np.zeros(256, np.float64)
+            d = np.zeros(256, np.uint8)
+            t0 = np.zeros(1, np.int32)
+            tk = np.zeros(k, np.int32)
+            cnt = np.zeros(1, np.int32)
+            st = self.lib.kref_pipeline(im.h, int(workers), int(k), _p(s), _p(c), _p(v), _p(d),
+                                        _p(t0), _p(tk), _p(cnt))
+            return dict(sum=s, card=c, values=v, defined=d, t0=int(t0[0]),
+                        topk=[int(t) for t in tk[: cnt[0]]], status=int(st))
+
+
+    def analyze_batch(self, imgs, k=6, workers=1, threads=None):
+        """Per-image pipeline over imgs[n, h, w], frame-parallel over `threads`
+        host threads (kref_pipeline_batch).  -> dict of stacked outputs."""
+        imgs = np.ascontiguousarray(imgs, dtype=np.uint8)
+        n = imgs.shape[0]
+        threads = threads or os.cpu_count() or 1
+        handles = [RefImage(self, imgs[i]) for i in range(n)]
+        arr = (C.c_void_p * n)(*[hh.h for hh in handles])
+        sums = np.zeros((n, 256), np.uint64)
+        cards = np.zeros((n, 256), np.uint64)
+        t0 = np.zeros(n, np.int32)
+        tk = np.zeros((n, k), np.int32)
+        cnt = np.zeros(n, np.int32)
+        self.lib.kref_pipeline_batch(arr, n, int(workers), int(threads), int(k), _p(sums),
+                                     _p(cards), _p(t0), _p(tk), _p(cnt))
+        for hh in handles:
+            hh.close()
+        return dict(sums=sums, cards=cards, t0=t0, topk=tk, topk_count=cnt)
+
+
+class RefImage:
+    """A kohler_ref::GrayImage built once (outside any timed region)."""
+
+    def __init__(self, ref: Reference, px):
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        self.ref = ref
+        self.h = ref.lib.kref_image_new(_p(px), px.shape[1], px.shape[0])
+        if not self.h:
+            raise ValueError("GrayImage: invalid dimensions")
+
+    def close(self):
+        if self.h:
+            self.ref.lib.kref_image_free(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,65 @@
+"""Row-band decomposition of one large image over the ranks of a
+``torch.distributed`` job (one process per GPU).
+
+Mirrors the reference's row-block split (proj/src/fast.cpp:42,53-55: block b
+of B owns rows [h*b/B, h*(b+1)/B)) and ownership rule (fast.cpp:15-31: a row
+owns its right pairs and the down pair into the next row), so each rank
+reads its rows plus ONE halo row.  Rank partials are exact integer curves of
+the pairs they own; one all-reduce (u64 sum carried as int64, two's
+complement) merges them like merge_accumulators (curve.cpp:16-30), then
+every rank runs the device selection on the merged curve.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def band_bounds(h: int, world: int, rank: int) -> tuple:
+    """Own rows [r0, r1) of `rank` (may be empty when world > h)."""
+    return (h * rank) // world, (h * (rank + 1)) // world
+
+
+def band_slice(h: int, r0: int, r1: int) -> tuple:
+    """Rows a rank must hold: its own rows plus the halo row r1 (if r1 < h)."""
+    return r0, min(r1 + 1, h)
+
+
+def allreduce_curve(buf: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum int64 curve partials [sum(256) | card(256)] over the group."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf
+
+
+class BandedAnalyzer:
+    """Per-rank driver: partial curve of the rank's band (K1 on the GPU),
+    NCCL all-reduce of the 512 u64 partials, device selection (K4)."""
+
+    def __init__(self, ctx, w: int, h: int, world: int, rank: int, k: int = 6, group=None):
+        self.ctx, self.w, self.h, self.k, self.group = ctx, w, h, k, group
+        self.r0, self.r1 = band_bounds(h, world, rank)
+        self.lo, self.hi = band_slice(h, self.r0, self.r1)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.curve = torch.zeros(512, dtype=torch.int64, device=dev)
+        self.out = {"values": torch.zeros(256, dtype=torch.float64, device=dev),
+                    "defined": torch.zeros(256, dtype=torch.uint8, device=dev),
+                    "t0": torch.zeros(1, dtype=torch.int32, device=dev),
+                    "topk": torch.zeros(k, dtype=torch.int32, device=dev),
+                    "topk_count": torch.zeros(1, dtype=torch.int32, device=dev),
+                    "status": torch.zeros(1, dtype=torch.int32, device=dev)}
+
+    @property
+    def rows_held(self) -> int:
+        return self.hi - self.lo
+
+    def step(self, band: torch.Tensor, pitch: int) -> None:
+        """band: CUDA uint8 buffer holding rows [lo, hi) with row pitch `pitch`."""
+        if self.r1 > self.r0:
+            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
+                                       self.curve.data_ptr(), self.curve.data_ptr() + 256 * 8)
+        else:
+            self.curve.zero_()
+        allreduce_curve(self.curve, self.group)
+        self.ctx.select_device(self.curve.data_ptr(), self.curve.data_ptr() + 256 * 8, 1, 256,
+                               self.k, self.out)

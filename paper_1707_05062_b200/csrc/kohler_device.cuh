@@ -1,0 +1,365 @@
+// kohler_device.cuh — device building blocks of the sm_100a Köhler path.
+//
+// Accumulation ("K1").  Every unordered 4-neighbour pair (a,b)
+// with lo = min, hi = max, s = a + b is reduced to O(1) integer updates:
+//     H_hi[hi] += 1, H_s[s] += 1            (per pair; equal pairs included)
+//     hist[a]  += 1                          (per pixel, as the 'cur' row)
+// The curve is rebuilt exactly from these:
+//     P      = 4*hist - corr                 (degree-weighted pixel histogram)
+//     card[t]= sum_{v<=t} (P[v] - 2 H_hi[v])
+//     sum[t] = sum_{u<=t} sum_{u'<=u} ( P[u'-1] - H_s[2u'-3] - 2 H_s[2u'-2] - H_s[2u'-1] )
+// because the tent min(hi-t, t-lo) on [lo,hi) (proj/src/kernels/pair_tent.hpp:12-18)
+// has second difference +1 at lo+1 and hi+1 and -1 at floor(s/2)+1 and
+// ceil(s/2)+1, and equal pairs cancel exactly.  `corr` holds the border
+// terms (missing neighbours) and the compensation for the equal "fake" pairs
+// the universal lane path creates at row ends (see process_step()).
+//
+// Histogram layout in shared memory (128 KiB, "lane-striped"): 512 rows of
+// 256 bytes; word (row, half, lane) lives at row*256 + half*128 + lane*4, so
+// lane L only ever touches bank L and every warp-wide update is
+// bank-conflict free whatever the keys are.  half 0 of row r holds H_s[r]
+// (r = 0..510), half 1 of rows 0..255 holds hist[v], half 1 of rows
+// 256..511 holds H_hi[v].  The byte address (key << 8) | lane*4 is one PRMT.
+#pragma once
+
+#include <cstdint>
+
+namespace kohler_dev {
+
+constexpr int kLevels = 256;
+constexpr uint32_t kStripedBytes = 512u * 256u;
+constexpr uint32_t kOffHs = 0;             // + (s << 8) | lane4
+constexpr uint32_t kOffHist = 128;         // + (v << 8) | lane4
+constexpr uint32_t kOffHhi = 65536 + 128;  // + (v << 8) | lane4
+
+__device__ __forceinline__ void inc(unsigned char* base, uint32_t off)
+{
+    atomicAdd(reinterpret_cast<uint32_t*>(base + off), 1u);
+}
+
+// Four pairs packed in 16-bit lanes: x = [a0, a2], y = [b0, b2] (one byte per
+// 16-bit lane, upper byte zero).  Two pairs per call.
+__device__ __forceinline__ void pairs2(unsigned char* sm, uint32_t x, uint32_t y, uint32_t lane4)
+{
+    const uint32_t hx = __vmaxu2(x, y);  // VIMNMX.U16x2
+    const uint32_t sx = x + y;           // no carry between halves (<= 510)
+    inc(sm + kOffHhi, __byte_perm(hx, lane4, 0x5504));
+    inc(sm + kOffHhi, __byte_perm(hx, lane4, 0x5524));
+    inc(sm + kOffHs, __byte_perm(sx, lane4, 0x5104));
+    inc(sm + kOffHs, __byte_perm(sx, lane4, 0x5324));
+}
+
+__device__ __forceinline__ void pixels4(unsigned char* sm, uint32_t c, uint32_t lane4)
+{
+    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5504));
+    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5514));
+    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5524));
+    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5534));
+}
+
+// All updates of one 16-pixel segment: 16 right pairs (the 16th against rn),
+// 16 down pairs (cur vs nxt) and 16 pixels.  80 conflict-free ATOMS.
+__device__ __forceinline__ void accumulate_segment(unsigned char* sm, const uint32_t (&c)[4],
+                                                   const uint32_t (&n)[4], uint32_t rn,
+                                                   uint32_t lane4)
+{
+    uint32_t ce[5];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        ce[j] = __byte_perm(c[j], 0, 0x4240);  // [b0, b2]
+    ce[4] = rn & 0xFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t co = __byte_perm(c[j], 0, 0x4341);          // [b1, b3]
+        const uint32_t ro = __byte_perm(ce[j], ce[j + 1], 0x1412); // [b2, next b0]
+        const uint32_t ne = __byte_perm(n[j], 0, 0x4240);
+        const uint32_t no = __byte_perm(n[j], 0, 0x4341);
+        pairs2(sm, ce[j], co, lane4);  // right pairs (b0,b1), (b2,b3)
+        pairs2(sm, co, ro, lane4);     // right pairs (b1,b2), (b3,next)
+        pairs2(sm, ce[j], ne, lane4);  // down pairs, columns 0 and 2
+        pairs2(sm, co, no, lane4);     // down pairs, columns 1 and 3
+        pixels4(sm, c[j], lane4);
+    }
+}
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t (&c)[4], int i)
+{
+    return (c[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+}
+
+// Replace bytes i > e of the segment by v (row-end lanes).
+__device__ __forceinline__ void fill_tail(uint32_t (&c)[4], int e, uint32_t v)
+{
+    const uint32_t vvvv = v * 0x01010101u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int keep = e - 4 * j + 1;  // bytes of word j to keep
+        if (keep <= 0)
+            c[j] = vvvv;
+        else if (keep < 4) {
+            const uint32_t m = 0xFFFFFFFFu << (8 * keep);
+            c[j] = (c[j] & ~m) | (vvvv & m);
+        }
+    }
+}
+
+template <bool VEC>
+__device__ __forceinline__ void load_segment(const uint8_t* row, int x0, int w, uint32_t (&c)[4])
+{
+    if (VEC) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
+        c[0] = v.x;
+        c[1] = v.y;
+        c[2] = v.z;
+        c[3] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int x = x0 + 4 * j + b;
+                const uint32_t byte = x < w ? __ldg(row + x) : 0u;
+                word |= byte << (8 * b);
+            }
+            c[j] = word;
+        }
+    }
+}
+
+// Geometry of one 16-pixel segment step, band-relative.
+struct StepGeom {
+    int w;         // image width
+    int y;         // band-relative row of `cur`
+    int band_rows; // own rows of the band
+    int gy;        // global row of `cur`
+    int h_total;   // global image height
+    int x0;        // first column of the segment
+};
+
+// One lane's step: fix up row ends / last rows so that every lane runs the
+// same predicate-free accumulate_segment, and record the border terms.
+//
+// Row-end lane (x0 + 16 >= w, e = w-1-x0): bytes > e of cur and nxt and the
+// right neighbour are replaced by v = cur[e].  The resulting equal "fake"
+// pairs cancel in the reconstruction once P counts them: the garbage pixels'
+// 4*hist supplies 4(15-e), the fake pairs need 2(16-e) + 2(15-e), so corr[v]
+// gets -2, plus +1 for pixel e's missing right pair: -1 in total.
+// Last image row: nxt := cur, so every down pair is an equal fake pair:
+// corr += 1 (missing down pair) - 2 (fake) = -1 per real pixel.
+// Band-first row: +1 per real pixel (its up pair belongs to the row above /
+// does not exist).  Row start: +1 (no left pair).  Halo row pixels (row r1 of
+// a band with r1 < h): -1 each (their up pair is owned, P gains 1).
+__device__ __forceinline__ void border_terms(int* corr, const StepGeom& g, uint32_t (&c)[4],
+                                             uint32_t (&n)[4], uint32_t& rn, bool has_down)
+{
+    const int e = g.w - 1 - g.x0;  // index of the last real pixel if < 16
+    const int last = e < 15 ? e : 15;
+    if (g.x0 == 0)
+        atomicAdd(&corr[c[0] & 0xFFu], 1);
+    if (g.y == 0)
+        for (int i = 0; i <= last; ++i)
+            atomicAdd(&corr[byte_of(c, i)], 1);
+    if (!has_down)
+        for (int i = 0; i <= last; ++i)
+            atomicAdd(&corr[byte_of(c, i)], -1);
+    else if (g.y + 1 == g.band_rows)
+        for (int i = 0; i <= last; ++i)
+            atomicAdd(&corr[byte_of(n, i)], -1);
+    if (e <= 15) {
+        const uint32_t v = byte_of(c, e);
+        fill_tail(c, e, v);
+        if (has_down)
+            fill_tail(n, e, v);
+        rn = v;
+        atomicAdd(&corr[v], -1);
+    }
+    if (!has_down) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            n[j] = c[j];
+    }
+}
+
+// ---- exact reconstruction ------------------------------------------------
+
+// Inclusive prefix over 256 int64 values by one warp (lane owns 8 entries).
+__device__ __forceinline__ void warp_prefix256(const long long* in, long long* out)
+{
+    const int lane = threadIdx.x & 31;
+    long long a[8];
+    long long run = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        run += in[lane * 8 + j];
+        a[j] = run;
+    }
+    long long x = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long yv = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off)
+            x += yv;
+    }
+    const long long excl = x - run;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        out[lane * 8 + j] = a[j] + excl;
+}
+
+// The 512 linear combinations one partial contributes: cd[v] (count first
+// difference) in [0,256) and h2[u] (sum second difference) in [256,512).
+// hist(v), hhi(v), hs(s) read the partial's reduced histograms.
+template <class Hist, class Hhi, class Hs, class Corr>
+__device__ __forceinline__ long long combo(int t, Hist hist, Hhi hhi, Hs hs, Corr corr)
+{
+    if (t < 256) {
+        const long long p = 4ll * (long long)hist(t) - (long long)corr(t);
+        return p - 2ll * (long long)hhi(t);
+    }
+    const int u = t - 256;
+    if (u == 0)
+        return 0;
+    const long long p = 4ll * (long long)hist(u - 1) - (long long)corr(u - 1);
+    long long r = p - 2ll * (long long)hs(2 * u - 2) - (long long)hs(2 * u - 1);
+    if (u >= 2)
+        r -= (long long)hs(2 * u - 3);
+    return r;
+}
+
+// ---- selection (K4): mean contrast, optimal threshold, top-k maxima ------
+
+struct SelectScratch {
+    double* rv;  // run values      [n]
+    int* rt;     // run first t     [n]
+    double* mv;  // maxima values   [n]
+    int* mt;     // maxima t        [n]
+};
+
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    return (1u << (threadIdx.x & 31)) - 1u;
+}
+
+// One warp selects on a curve held in shared (or global) memory.
+// Restates proj/src/threshold.cpp:25-82 exactly (for non-NaN values):
+// optimal_threshold = argmax with ties to the smallest t; top_k_local_maxima
+// collapses equal-valued runs of the defined subsequence to their first t,
+// keeps runs strictly above both neighbouring runs (one-sided at the ends),
+// ranks by (value desc, t asc), keeps k, outputs ascending.
+// Returns 1 (no boundary) when nothing is defined, else 0.
+__device__ int warp_select(const double* val, const uint8_t* def, int n, int k,
+                           const SelectScratch& s, int* out_t0, int* out_topk, int* out_count)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+
+    double bv = 0.0;
+    int bt = -1;
+    for (int t = lane; t < n; t += 32) {
+        if (def[t]) {
+            const double v = val[t];
+            if (bt < 0 || v > bv) {
+                bv = v;
+                bt = t;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, off);
+        const int ot = __shfl_xor_sync(0xFFFFFFFFu, bt, off);
+        if (ot >= 0 && (bt < 0 || ov > bv || (ov == bv && ot < bt))) {
+            bv = ov;
+            bt = ot;
+        }
+    }
+
+    bool carry_has = false;
+    double carry_v = 0.0;
+    int nr = 0;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int t = c0 + lane;
+        const bool d = t < n && def[t];
+        const double v = d ? val[t] : 0.0;
+        const unsigned dm = __ballot_sync(0xFFFFFFFFu, d);
+        const unsigned before = dm & lt;
+        const int src = before ? 31 - __clz(before) : lane;
+        const double pv_lane = __shfl_sync(0xFFFFFFFFu, v, src);
+        const bool has_prev = before != 0 || carry_has;
+        const double pv = before ? pv_lane : carry_v;
+        const bool start = d && (!has_prev || v != pv);
+        const unsigned sm = __ballot_sync(0xFFFFFFFFu, start);
+        if (start) {
+            const int pos = nr + __popc(sm & lt);
+            s.rv[pos] = v;
+            s.rt[pos] = t;
+        }
+        nr += __popc(sm);
+        if (dm) {
+            carry_v = __shfl_sync(0xFFFFFFFFu, v, 31 - __clz(dm));
+            carry_has = true;
+        }
+    }
+    __syncwarp();
+    if (nr == 0) {
+        if (lane == 0) {
+            if (out_t0)
+                *out_t0 = -1;
+            if (out_count)
+                *out_count = 0;
+        }
+        return 1;
+    }
+
+    int nm = 0;
+    for (int r0 = 0; r0 < nr; r0 += 32) {
+        const int r = r0 + lane;
+        bool m = false;
+        double v = 0.0;
+        int t = 0;
+        if (r < nr) {
+            v = s.rv[r];
+            t = s.rt[r];
+            m = (r == 0 || v > s.rv[r - 1]) && (r == nr - 1 || v > s.rv[r + 1]);
+        }
+        const unsigned mm = __ballot_sync(0xFFFFFFFFu, m);
+        if (m) {
+            const int pos = nm + __popc(mm & lt);
+            s.mv[pos] = v;
+            s.mt[pos] = t;
+        }
+        nm += __popc(mm);
+    }
+    __syncwarp();
+
+    int cnt = 0;
+    for (int i0 = 0; i0 < nm; i0 += 32) {
+        const int i = i0 + lane;
+        bool sel = false;
+        int ti = 0;
+        if (i < nm) {
+            const double v = s.mv[i];
+            ti = s.mt[i];
+            int rank = 0;
+            for (int j = 0; j < nm && rank < k; ++j) {
+                const double u = s.mv[j];
+                rank += (u > v) || (u == v && s.mt[j] < ti);
+            }
+            sel = rank < k;
+        }
+        const unsigned sb = __ballot_sync(0xFFFFFFFFu, sel);
+        if (sel && out_topk)
+            out_topk[cnt + __popc(sb & lt)] = ti;
+        cnt += __popc(sb);
+    }
+    if (lane == 0) {
+        if (out_t0)
+            *out_t0 = bt;
+        if (out_count)
+            *out_count = cnt;
+    }
+    return 0;
+}
+
+} // namespace kohler_dev

@@ -1,0 +1,973 @@
+// kohler_kernels.cu — sm_100a kernels of the Köhler contrast-curve path and
+// the C ABI (include/kohler_cuda.h) that launches them.
+//
+//   K1  wide_kernel    : persistent, one 1024-thread CTA per SM; each CTA owns
+//                        a contiguous range of 16-pixel segments (flattened
+//                        row-major over the batch), accumulates them into a
+//                        lane-striped 128 KiB shared histogram (kohler_device.cuh),
+//                        and at every image boundary flushes 512 exact linear
+//                        combinations to global u64 accumulators (REDG.ADD.64).
+//   K3  (tail of K1)   : the last CTA to flush an image (atomic ticket) sums
+//                        the accumulator copies, rebuilds count/sum with int64
+//                        prefix scans and resets the workspace for the next launch.
+//   K4  (tail of K1) / select_kernel : mean curve (IEEE f64 divide), optimal
+//                        threshold, top-k local maxima, on device.
+//
+// The whole per-image pipeline is therefore ONE launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kohler_cuda.h"
+#include "kohler_device.cuh"
+
+using namespace kohler_dev;
+
+namespace {
+
+constexpr int kWideThreads = 1024;
+constexpr int kWideWarps = kWideThreads / 32;
+constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
+constexpr int kMaxSelectLevels = 4096;
+
+struct WideParams {
+    const uint8_t* px;
+    size_t pitch;
+    size_t image_stride;
+    int n;          // images
+    int w;          // width
+    int band_rows;  // own rows per image (band)
+    int h_total;    // global height
+    int r0;         // global row of buffer row 0
+    int nseg;       // 16-pixel segments per row
+    long long upi;  // units (32 segments) per image
+    long long total_units;
+    unsigned long long* acc;  // [n][copies][512]
+    int copies;
+    unsigned* tickets;  // [n]
+    int k;
+    int select;
+    uint64_t* sums;
+    uint64_t* cards;
+    double* values;
+    uint8_t* defined;
+    int* t0s;
+    int* topks;
+    int* topk_counts;
+    int* status;
+};
+
+// Shared-memory map of K1 (dynamic).
+constexpr uint32_t kSmCorr = kStripedBytes;                 // int[256]
+constexpr uint32_t kSmCorrCopy = kSmCorr + 1024;            // int[256]
+constexpr uint32_t kSmTot = kSmCorrCopy + 1024;             // u64[1024]
+constexpr uint32_t kSmVal = kSmTot + 8192;                  // i64[512]
+constexpr uint32_t kSmCurve = kSmVal + 4096;                // u64 sum[256], card[256]
+constexpr uint32_t kSmMean = kSmCurve + 4096;               // f64[256]
+constexpr uint32_t kSmDef = kSmMean + 2048;                 // u8[256]
+constexpr uint32_t kSmScratch = kSmDef + 256;               // rv,rt,mv,mt [256]
+constexpr uint32_t kSmWideBytes = kSmScratch + 256 * (8 + 4 + 8 + 4);
+
+__device__ __forceinline__ long long cta_of_unit(long long u, long long G, long long U)
+{
+    return ((u + 1) * G - 1) / U;
+}
+
+// Last CTA of an image: sum accumulator copies, reset them, rebuild the
+// curve, write it, and (optionally) select.
+__device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
+{
+    const int tid = threadIdx.x;
+    long long* sval = reinterpret_cast<long long*>(sm + kSmVal);
+    uint64_t* csum = reinterpret_cast<uint64_t*>(sm + kSmCurve);
+    uint64_t* ccard = csum + 256;
+    double* mean = reinterpret_cast<double*>(sm + kSmMean);
+    uint8_t* def = sm + kSmDef;
+
+    if (tid < 512) {
+        unsigned long long* a = p.acc + (size_t)img * p.copies * 512;
+        unsigned long long s = 0;
+        for (int c = 0; c < p.copies; ++c) {
+            s += __ldcg(a + c * 512 + tid);
+            __stcg(a + c * 512 + tid, 0ull);
+        }
+        sval[tid] = (long long)s;
+    }
+    if (tid == 0)
+        p.tickets[img] = 0;
+    __syncthreads();
+    const int warp = tid >> 5;
+    long long* tmp = reinterpret_cast<long long*>(sm + kSmTot);  // reuse
+    if (warp == 0)
+        warp_prefix256(sval, reinterpret_cast<long long*>(ccard));
+    else if (warp == 1) {
+        warp_prefix256(sval + 256, tmp);
+        __syncwarp();
+        warp_prefix256(tmp, reinterpret_cast<long long*>(csum));
+    }
+    __syncthreads();
+    if (tid < 256) {
+        const uint64_t cs = csum[tid], cc = ccard[tid];
+        const double v = cc ? (double)cs / (double)cc : 0.0;
+        mean[tid] = v;
+        def[tid] = cc ? 1 : 0;
+        if (p.sums) {
+            p.sums[(size_t)img * 256 + tid] = cs;
+            p.cards[(size_t)img * 256 + tid] = cc;
+        }
+        if (p.values)
+            p.values[(size_t)img * 256 + tid] = v;
+        if (p.defined)
+            p.defined[(size_t)img * 256 + tid] = cc ? 1 : 0;
+    }
+    __syncthreads();
+    if (p.select && warp == 0) {
+        unsigned char* scr = sm + kSmScratch;
+        SelectScratch s{reinterpret_cast<double*>(scr), reinterpret_cast<int*>(scr + 2048),
+                        reinterpret_cast<double*>(scr + 3072), reinterpret_cast<int*>(scr + 5120)};
+        const int st = warp_select(mean, def, 256, p.k, s, p.t0s ? p.t0s + img : nullptr,
+                                   p.topks ? p.topks + (size_t)img * p.k : nullptr,
+                                   p.topk_counts ? p.topk_counts + img : nullptr);
+        if (tid == 0 && p.status)
+            p.status[img] = st;
+    }
+}
+
+// CTA flush of one image's partial: reduce the striped histogram (zeroing it
+// for the next image), form the 512 combinations, REDG them, take a ticket.
+__device__ void flush_image(const WideParams& p, int img, unsigned char* sm, long long G,
+                            long long U)
+{
+    const int tid = threadIdx.x;
+    int* corr = reinterpret_cast<int*>(sm + kSmCorr);
+    int* corr_copy = reinterpret_cast<int*>(sm + kSmCorrCopy);
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(sm + kSmTot);
+
+    {
+        // thread t owns (row t>>1, half t&1): 32 lane words, read rotated
+        // by t&7 so a warp's LDS.128 hit distinct bank quads.
+        uint4* row = reinterpret_cast<uint4*>(sm + (tid >> 1) * 256 + (tid & 1) * 128);
+        unsigned long long s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = (j + tid) & 7;
+            const uint4 v = row[q];
+            s += (unsigned long long)v.x + v.y + v.z + v.w;
+            row[q] = make_uint4(0, 0, 0, 0);
+        }
+        tot[tid] = s;
+        if (tid < 256) {
+            corr_copy[tid] = corr[tid];
+            corr[tid] = 0;
+        }
+    }
+    __syncthreads();
+    if (tid < 512) {
+        const long long v = combo(
+            tid, [&](int x) { return tot[2 * x + 1]; },
+            [&](int x) { return tot[2 * (256 + x) + 1]; }, [&](int x) { return tot[2 * x]; },
+            [&](int x) { return corr_copy[x]; });
+        if (v != 0) {
+            const int copy = blockIdx.x % p.copies;
+            atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + tid,
+                      (unsigned long long)v);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (tid == 0) {
+        const long long first = cta_of_unit((long long)img * p.upi, G, U);
+        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, G, U);
+        const unsigned expected = (unsigned)(last - first + 1);
+        const unsigned prev = atomicAdd(p.tickets + img, 1u);
+        s_last = (prev + 1 == expected);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        finish_image(p, img, sm);
+    }
+    __syncthreads();
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams p)
+{
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const uint32_t lane4 = (uint32_t)lane * 4u;
+    int* corr = reinterpret_cast<int*>(sm + kSmCorr);
+
+    {
+        uint4* z = reinterpret_cast<uint4*>(sm);
+        for (int i = tid; i < (int)(kStripedBytes / 16); i += kWideThreads)
+            z[i] = make_uint4(0, 0, 0, 0);
+        if (tid < 256)
+            corr[tid] = 0;
+    }
+    __syncthreads();
+
+    const long long U = p.total_units;
+    const long long G = gridDim.x;
+    const long long cs = U * blockIdx.x / G;
+    const long long ce = U * (blockIdx.x + 1) / G;
+    if (cs >= ce)
+        return;
+    const int i_first = (int)(cs / p.upi);
+    const int i_last = (int)((ce - 1) / p.upi);
+    const long long nseg_img = (long long)p.band_rows * p.nseg;
+    const int nseg = p.nseg;
+    const int w = p.w;
+
+    for (int img = i_first; img <= i_last; ++img) {
+        const long long ibase = (long long)img * p.upi;
+        const long long a = cs > ibase ? cs : ibase;
+        const long long b = ce < ibase + p.upi ? ce : ibase + p.upi;
+        const long long len = b - a;
+        const long long wa = a + len * warp / kWideWarps;
+        const long long wb = a + len * (warp + 1) / kWideWarps;
+        const uint8_t* base = p.px + (size_t)img * p.image_stride;
+
+        if (wa < wb) {
+            long long g = (wa - ibase) * 32 + lane;
+            int y = (int)(g / nseg);
+            int seg = (int)(g - (long long)y * nseg);
+            for (long long u = wa; u < wb; ++u) {
+                const bool active = g < nseg_img;
+                const int x0 = seg * 16;
+                const uint8_t* row = base + (size_t)y * p.pitch;
+                const int gy = p.r0 + y;
+                const bool has_down = gy + 1 < p.h_total;
+                uint32_t c[4] = {0, 0, 0, 0}, nx[4] = {0, 0, 0, 0};
+                uint32_t rn = 0;
+                if (active) {
+                    load_segment<VEC>(row, x0, w, c);
+                    if (has_down)
+                        load_segment<VEC>(row + p.pitch, x0, w, nx);
+                    if (lane == 31 && x0 + 16 < w)
+                        rn = __ldg(row + x0 + 16);
+                }
+                const uint32_t sh = __shfl_down_sync(0xFFFFFFFFu, c[0] & 0xFFu, 1);
+                if (lane < 31)
+                    rn = sh;
+                if (active) {
+                    const bool interior = (x0 != 0) && (x0 + 16 < w) && has_down && (y != 0) &&
+                                          (y + 1 != p.band_rows);
+                    if (!interior) {
+                        StepGeom geom{w, y, p.band_rows, gy, p.h_total, x0};
+                        border_terms(corr, geom, c, nx, rn, has_down);
+                    }
+                    accumulate_segment(sm, c, nx, rn, lane4);
+                }
+                g += 32;
+                seg += 32;
+                if (seg >= nseg) {
+                    if (nseg >= 32) {
+                        seg -= nseg;
+                        ++y;
+                    } else {
+                        y += seg / nseg;
+                        seg %= nseg;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        flush_image(p, img, sm, G, U);
+    }
+}
+
+// Definition-level oracle kernel: block t scans every
+// ordered 4-neighbour pair (x0 <= t < x1) of the image, like
+// proj/src/direct.cpp:18-38.  Shares nothing with K1.  out: sum[256], card[256].
+__global__ void __launch_bounds__(256) direct_kernel(const uint8_t* px, int w, int h, size_t pitch,
+                                                     unsigned long long* out)
+{
+    const int t = blockIdx.x;
+    unsigned long long s = 0, c = 0;
+    const long long npx = (long long)w * h;
+    for (long long i = threadIdx.x; i < npx; i += blockDim.x) {
+        const int y = (int)(i / w), x = (int)(i - (long long)y * w);
+        const int v0 = px[(size_t)y * pitch + x];
+        if (v0 > t)
+            continue;
+        const int dx[4] = {1, -1, 0, 0};
+        const int dy[4] = {0, 0, 1, -1};
+        for (int d = 0; d < 4; ++d) {
+            const int x1 = x + dx[d], y1 = y + dy[d];
+            if (x1 < 0 || x1 >= w || y1 < 0 || y1 >= h)
+                continue;
+            const int v1 = px[(size_t)y1 * pitch + x1];
+            if (v1 > t) {
+                c += 1;
+                s += (unsigned long long)min(v1 - t, t - v0);
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+        c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
+    }
+    __shared__ unsigned long long ws[8], wc[8];
+    if ((threadIdx.x & 31) == 0) {
+        ws[threadIdx.x >> 5] = s;
+        wc[threadIdx.x >> 5] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long ts = 0, tc = 0;
+        for (int i = 0; i < 8; ++i) {
+            ts += ws[i];
+            tc += wc[i];
+        }
+        out[t] = ts;
+        out[256 + t] = tc;
+    }
+}
+
+// Standalone selection: one warp per curve.  mode 0: input (sum, card);
+// mode 1: input (values, defined).
+struct SelectParams {
+    const uint64_t* sums;
+    const uint64_t* cards;
+    const double* in_values;
+    const uint8_t* in_defined;
+    int n_curves;
+    int levels;
+    int k;
+    int want_select;  // 0: only values/defined
+    double* values;
+    uint8_t* defined;
+    int* t0s;
+    int* topks;
+    int* topk_counts;
+    int* status;
+};
+
+__global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
+{
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int n = p.levels;
+    const int cidx = blockIdx.x;
+    double* val = reinterpret_cast<double*>(sm);
+    double* rv = val + n;
+    double* mv = rv + n;
+    int* rt = reinterpret_cast<int*>(mv + n);
+    int* mt = rt + n;
+    uint8_t* def = reinterpret_cast<uint8_t*>(mt + n);
+    const size_t off = (size_t)cidx * n;
+    for (int t = threadIdx.x; t < n; t += 32) {
+        double v;
+        uint8_t d;
+        if (p.sums) {
+            const uint64_t cc = p.cards[off + t];
+            v = cc ? (double)p.sums[off + t] / (double)cc : 0.0;
+            d = cc ? 1 : 0;
+        } else {
+            v = p.in_values[off + t];
+            d = p.in_defined[off + t] ? 1 : 0;
+        }
+        val[t] = v;
+        def[t] = d;
+        if (p.values)
+            p.values[off + t] = v;
+        if (p.defined)
+            p.defined[off + t] = d;
+    }
+    __syncwarp();
+    if (!p.want_select)
+        return;
+    SelectScratch s{rv, rt, mv, mt};
+    const int st = warp_select(val, def, n, p.k, s, p.t0s ? p.t0s + cidx : nullptr,
+                               p.topks ? p.topks + (size_t)cidx * p.k : nullptr,
+                               p.topk_counts ? p.topk_counts + cidx : nullptr);
+    if (threadIdx.x == 0 && p.status)
+        p.status[cidx] = st;
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg)
+{
+    g_last_error = msg;
+    return code;
+}
+
+#define KC_CUDA(call)                                                                    \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(e_ == cudaErrorMemoryAllocation ? KOHLER_OUT_OF_MEMORY           \
+                                                        : KOHLER_CUDA_ERROR,             \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes, bool zero = false)
+    {
+        if (bytes <= cap)
+            return KOHLER_OK;
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        KC_CUDA(cudaMalloc(&p, bytes));
+        if (zero)
+            KC_CUDA(cudaMemset(p, 0, bytes));
+        cap = bytes;
+        return KOHLER_OK;
+    }
+    void release()
+    {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+} // namespace
+
+struct kohler_cuda_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    DevBuf acc;      // zero-initialised, self-cleaning
+    DevBuf tickets;  // zero-initialised, self-cleaning
+    DevBuf img;      // staging for host images
+    DevBuf out;      // staging for host outputs
+    int last_launches = 0;
+    bool wide_attr_set = false;
+    bool select_attr_set = false;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+struct BatchOut {
+    uint64_t* sums;
+    uint64_t* cards;
+    double* values;
+    uint8_t* defined;
+    int* t0s;
+    int* topks;
+    int* topk_counts;
+    int* status;
+};
+
+int check_image(int n, int w, int h, size_t pitch)
+{
+    if (n < 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "image count must be >= 0");
+    if (w < 1 || h < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "GrayImage: dimensions must be at least 1x1");
+    if (pitch < (size_t)w)
+        return fail(KOHLER_INVALID_ARGUMENT, "row pitch must be >= width");
+    return KOHLER_OK;
+}
+
+// Launch K1 over n images whose buffers hold band_rows own rows (+ halo).
+int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
+                int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
+                const BatchOut& o, cudaStream_t stream)
+{
+    if (n == 0)
+        return KOHLER_OK;
+    const int nseg = (w + 15) / 16;
+    const long long segs = (long long)band_rows * nseg;
+    const long long upi = (segs + 31) / 32;
+    const long long U = upi * n;
+    long long G = (U + 63) / 64;
+    G = std::max(1ll, std::min<long long>(G, ctx->sm_count));
+    const int copies = n == 1 ? kAccCopiesSingle : 1;
+    int rc = ctx->acc.ensure((size_t)n * copies * 512 * sizeof(unsigned long long), true);
+    if (rc)
+        return rc;
+    rc = ctx->tickets.ensure((size_t)n * sizeof(unsigned), true);
+    if (rc)
+        return rc;
+
+    WideParams p{};
+    p.px = px;
+    p.pitch = pitch;
+    p.image_stride = image_stride;
+    p.n = n;
+    p.w = w;
+    p.band_rows = band_rows;
+    p.h_total = h_total;
+    p.r0 = r0;
+    p.nseg = nseg;
+    p.upi = upi;
+    p.total_units = U;
+    p.acc = static_cast<unsigned long long*>(ctx->acc.p);
+    p.copies = copies;
+    p.tickets = static_cast<unsigned*>(ctx->tickets.p);
+    p.k = k;
+    p.select = select;
+    p.sums = o.sums;
+    p.cards = o.cards;
+    p.values = o.values;
+    p.defined = o.defined;
+    p.t0s = o.t0s;
+    p.topks = o.topks;
+    p.topk_counts = o.topk_counts;
+    p.status = o.status;
+
+    const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
+                     (n == 1 || image_stride % 16 == 0);
+    // the smem opt-in is per device; remember it per context
+    if (!ctx->wide_attr_set) {
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        ctx->wide_attr_set = true;
+    }
+    if (vec)
+        wide_kernel<true><<<(unsigned)G, kWideThreads, kSmWideBytes, stream>>>(p);
+    else
+        wide_kernel<false><<<(unsigned)G, kWideThreads, kSmWideBytes, stream>>>(p);
+    KC_CUDA(cudaGetLastError());
+    ctx->last_launches += 1;
+    return KOHLER_OK;
+}
+
+int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t stream)
+{
+    if (sp.n_curves == 0)
+        return KOHLER_OK;
+    const size_t smem = (size_t)sp.levels * (8 * 3 + 4 * 2 + 1);
+    if (!ctx->select_attr_set) {
+        KC_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kMaxSelectLevels * (8 * 3 + 4 * 2 + 1))));
+        ctx->select_attr_set = true;
+    }
+    select_kernel<<<sp.n_curves, 32, smem, stream>>>(sp);
+    KC_CUDA(cudaGetLastError());
+    ctx->last_launches += 1;
+    return KOHLER_OK;
+}
+
+// Stage a host batch into the device, run, copy results back.
+int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
+               size_t image_stride, int k, int select, const BatchOut& host)
+{
+    const size_t dpitch = round_up((size_t)w, 128);
+    const size_t dstride = dpitch * (size_t)h;
+    int rc = ctx->img.ensure(std::max<size_t>(dstride * (size_t)n, 16));
+    if (rc)
+        return rc;
+    uint8_t* dimg = static_cast<uint8_t*>(ctx->img.p);
+    cudaStream_t st = ctx->stream;
+    if (image_stride == pitch * (size_t)h) {
+        KC_CUDA(cudaMemcpy2DAsync(dimg, dpitch, px, pitch, (size_t)w, (size_t)h * n,
+                                  cudaMemcpyHostToDevice, st));
+    } else {
+        for (int i = 0; i < n; ++i)
+            KC_CUDA(cudaMemcpy2DAsync(dimg + dstride * i, dpitch, px + image_stride * i, pitch,
+                                      (size_t)w, (size_t)h, cudaMemcpyHostToDevice, st));
+    }
+    // device outputs, packed
+    const size_t n256 = (size_t)n * 256;
+    const size_t bytes = n256 * 8 * 3 + n256 + (size_t)n * 4 * 4 + (size_t)n * k * 4 + 64;
+    rc = ctx->out.ensure(bytes);
+    if (rc)
+        return rc;
+    char* b = static_cast<char*>(ctx->out.p);
+    BatchOut d{};
+    d.sums = host.sums ? reinterpret_cast<uint64_t*>(b) : nullptr;
+    d.cards = host.cards ? reinterpret_cast<uint64_t*>(b + n256 * 8) : nullptr;
+    if (d.sums && !d.cards)
+        d.cards = reinterpret_cast<uint64_t*>(b + n256 * 8);
+    if (d.cards && !d.sums)
+        d.sums = reinterpret_cast<uint64_t*>(b);
+    d.values = host.values ? reinterpret_cast<double*>(b + n256 * 16) : nullptr;
+    d.defined = host.defined ? reinterpret_cast<uint8_t*>(b + n256 * 24) : nullptr;
+    char* tail = b + n256 * 25;
+    tail = reinterpret_cast<char*>(round_up(reinterpret_cast<uintptr_t>(tail), 16));
+    d.t0s = reinterpret_cast<int*>(tail);
+    d.topk_counts = d.t0s + n;
+    d.status = d.topk_counts + n;
+    d.topks = d.status + n;
+    ctx->last_launches = 0;
+    rc = launch_wide(ctx, dimg, n, w, h, h, 0, dpitch, dstride, k, select, d, st);
+    if (rc)
+        return rc;
+    if (host.sums)
+        KC_CUDA(cudaMemcpyAsync(host.sums, d.sums, n256 * 8, cudaMemcpyDeviceToHost, st));
+    if (host.cards)
+        KC_CUDA(cudaMemcpyAsync(host.cards, d.cards, n256 * 8, cudaMemcpyDeviceToHost, st));
+    if (host.values)
+        KC_CUDA(cudaMemcpyAsync(host.values, d.values, n256 * 8, cudaMemcpyDeviceToHost, st));
+    if (host.defined)
+        KC_CUDA(cudaMemcpyAsync(host.defined, d.defined, n256, cudaMemcpyDeviceToHost, st));
+    if (select) {
+        if (host.t0s)
+            KC_CUDA(cudaMemcpyAsync(host.t0s, d.t0s, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        if (host.topk_counts)
+            KC_CUDA(cudaMemcpyAsync(host.topk_counts, d.topk_counts, (size_t)n * 4,
+                                    cudaMemcpyDeviceToHost, st));
+        if (host.status)
+            KC_CUDA(cudaMemcpyAsync(host.status, d.status, (size_t)n * 4,
+                                    cudaMemcpyDeviceToHost, st));
+        if (host.topks)
+            KC_CUDA(cudaMemcpyAsync(host.topks, d.topks, (size_t)n * k * 4,
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    KC_CUDA(cudaStreamSynchronize(st));
+    return KOHLER_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int kohler_cuda_abi_version(void) { return 100; }
+
+const char* kohler_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int kohler_cuda_create(int device, kohler_cuda_ctx** out)
+{
+    if (!out)
+        return fail(KOHLER_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    KC_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0)
+        KC_CUDA(cudaGetDevice(&device));
+    if (device >= ndev)
+        return fail(KOHLER_INVALID_ARGUMENT, "no such CUDA device");
+    DeviceGuard g(device);
+    int major = 0, minor = 0;
+    KC_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    KC_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+        return fail(KOHLER_CUDA_ERROR, "this build targets sm_100a (B200) only; device is sm_" +
+                                           std::to_string(major) + std::to_string(minor));
+    auto* ctx = new kohler_cuda_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fail(KOHLER_CUDA_ERROR, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return KOHLER_OK;
+}
+
+void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
+{
+    if (!ctx)
+        return;
+    {
+        DeviceGuard g(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->acc.release();
+        ctx->tickets.release();
+        ctx->img.release();
+        ctx->out.release();
+        cudaStreamDestroy(ctx->stream);
+    }
+    delete ctx;
+}
+
+int kohler_cuda_device(const kohler_cuda_ctx* ctx) { return ctx ? ctx->device : -1; }
+
+int kohler_cuda_last_launch_count(const kohler_cuda_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int kohler_cuda_curve(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                      uint64_t* sum, uint64_t* card)
+{
+    if (!ctx || !px || !sum || !card)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(1, w, h, pitch);
+    if (rc)
+        return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    BatchOut o{sum, card, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return host_batch(ctx, px, 1, w, h, pitch, pitch * (size_t)h, 1, 0, o);
+}
+
+int kohler_cuda_direct_curve(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                             uint64_t* sum, uint64_t* card)
+{
+    if (!ctx || !px || !sum || !card)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(1, w, h, pitch);
+    if (rc)
+        return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t bytes = (size_t)w * h;
+    rc = ctx->img.ensure(std::max<size_t>(bytes, 16));
+    if (rc)
+        return rc;
+    rc = ctx->out.ensure(512 * sizeof(unsigned long long));
+    if (rc)
+        return rc;
+    uint8_t* dimg = static_cast<uint8_t*>(ctx->img.p);
+    auto* dout = static_cast<unsigned long long*>(ctx->out.p);
+    KC_CUDA(cudaMemcpy2DAsync(dimg, (size_t)w, px, pitch, (size_t)w, (size_t)h,
+                              cudaMemcpyHostToDevice, st));
+    ctx->last_launches = 1;
+    direct_kernel<<<256, 256, 0, st>>>(dimg, w, h, (size_t)w, dout);
+    KC_CUDA(cudaGetLastError());
+    KC_CUDA(cudaMemcpyAsync(sum, dout, 256 * 8, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaMemcpyAsync(card, dout + 256, 256 * 8, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaStreamSynchronize(st));
+    return KOHLER_OK;
+}
+
+int kohler_cuda_analyze(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                        int k, uint64_t* sum, uint64_t* card, double* values, uint8_t* defined,
+                        int* t0, int* topk, int* topk_count)
+{
+    int status = 0;
+    const int rc = kohler_cuda_analyze_batch(ctx, px, 1, w, h, pitch, pitch * (size_t)h, k, sum,
+                                             card, values, defined, t0, topk, topk_count, &status);
+    if (rc)
+        return rc;
+    return status;
+}
+
+int kohler_cuda_analyze_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h,
+                              size_t pitch, size_t image_stride, int k, uint64_t* sums,
+                              uint64_t* cards, double* values, uint8_t* defined, int* t0s,
+                              int* topks, int* topk_counts, int* status)
+{
+    if (!ctx || (!px && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(n, w, h, pitch);
+    if (rc)
+        return rc;
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (n > 1 && image_stride < pitch * (size_t)h)
+        return fail(KOHLER_INVALID_ARGUMENT, "image stride smaller than one image");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
+    return host_batch(ctx, px, n, w, h, pitch, image_stride, k, 1, o);
+}
+
+int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w,
+                                     int h, size_t pitch, size_t image_stride, int k,
+                                     uint64_t* sums, uint64_t* cards, double* values,
+                                     uint8_t* defined, int* t0s, int* topks, int* topk_counts,
+                                     int* status, void* stream)
+{
+    if (!ctx || (!px && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(n, w, h, pitch);
+    if (rc)
+        return rc;
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (n > 1 && image_stride < pitch * (size_t)h)
+        return fail(KOHLER_INVALID_ARGUMENT, "image stride smaller than one image");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
+    const bool select = t0s || topks || topk_counts || status;
+    return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select ? 1 : 0, o,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_band_curve_device(kohler_cuda_ctx* ctx, const uint8_t* band, int w, size_t pitch,
+                                  int h_total, int r0, int r1, uint64_t* sum, uint64_t* card,
+                                  void* stream)
+{
+    if (!ctx || !band || !sum || !card)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(1, w, h_total, pitch);
+    if (rc)
+        return rc;
+    if (r0 < 0 || r1 <= r0 || r1 > h_total)
+        return fail(KOHLER_INVALID_ARGUMENT, "band rows must satisfy 0 <= r0 < r1 <= h");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    BatchOut o{sum, card, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return launch_wide(ctx, band, 1, w, r1 - r0, h_total, r0, pitch, 0, 1, 0, o,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_select_device(kohler_cuda_ctx* ctx, const uint64_t* sums, const uint64_t* cards,
+                              int n_curves, int levels, int k, double* values, uint8_t* defined,
+                              int* t0s, int* topks, int* topk_counts, int* status, void* stream)
+{
+    if (!ctx || (n_curves > 0 && (!sums || !cards)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    if (levels < 1 || levels > kMaxSelectLevels)
+        return fail(KOHLER_INVALID_ARGUMENT, "levels must be in [1, 4096]");
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    SelectParams sp{sums,  cards,   nullptr, nullptr, n_curves,    levels, k,
+                    1,     values,  defined, t0s,     topks,       topk_counts, status};
+    return launch_select(ctx, sp, static_cast<cudaStream_t>(stream));
+}
+
+// Host-curve selection helpers (drop-in mean_contrast / optimal_threshold /
+// top_k_local_maxima): stage, run select_kernel, copy back.
+static int host_select(kohler_cuda_ctx* ctx, const uint64_t* sum, const uint64_t* card,
+                       const double* values_in, const uint8_t* defined_in, int n, int k,
+                       double* values, uint8_t* defined, int* t0, int* topk, int* count,
+                       int* status_out)
+{
+    if (n < 0 || n > kMaxSelectLevels)
+        return fail(KOHLER_INVALID_ARGUMENT, "levels must be in [0, 4096]");
+    if (n == 0) {
+        if (t0)
+            *t0 = -1;
+        if (count)
+            *count = 0;
+        if (status_out)
+            *status_out = KOHLER_NO_BOUNDARY;
+        return KOHLER_OK;
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const size_t need = (size_t)n * (8 + 8 + 1 + 1 + 8) + (size_t)k * 4 + 64;
+    int rc = ctx->out.ensure(need);
+    if (rc)
+        return rc;
+    char* b = static_cast<char*>(ctx->out.p);
+    uint64_t* dsum = reinterpret_cast<uint64_t*>(b);
+    uint64_t* dcard = dsum + n;
+    double* dval = reinterpret_cast<double*>(dcard + n);
+    uint8_t* ddef = reinterpret_cast<uint8_t*>(dval + n);
+    int* dint = reinterpret_cast<int*>(round_up(reinterpret_cast<uintptr_t>(ddef + n), 16));
+    SelectParams sp{};
+    sp.n_curves = 1;
+    sp.levels = n;
+    sp.k = k;
+    if (sum) {
+        KC_CUDA(cudaMemcpyAsync(dsum, sum, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        KC_CUDA(cudaMemcpyAsync(dcard, card, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        sp.sums = dsum;
+        sp.cards = dcard;
+        sp.values = dval;
+        sp.defined = ddef;
+        sp.want_select = 0;
+    } else {
+        // values/defined in: reuse dsum/dcard space
+        double* vin = reinterpret_cast<double*>(dsum);
+        uint8_t* din = reinterpret_cast<uint8_t*>(dcard);
+        KC_CUDA(cudaMemcpyAsync(vin, values_in, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        KC_CUDA(cudaMemcpyAsync(din, defined_in, (size_t)n, cudaMemcpyHostToDevice, st));
+        sp.in_values = vin;
+        sp.in_defined = din;
+        sp.want_select = 1;
+        sp.t0s = dint;
+        sp.topk_counts = dint + 1;
+        sp.status = dint + 2;
+        sp.topks = dint + 4;
+    }
+    ctx->last_launches = 0;
+    rc = launch_select(ctx, sp, st);
+    if (rc)
+        return rc;
+    int hint[4] = {0, 0, 0, 0};
+    if (sum) {
+        KC_CUDA(cudaMemcpyAsync(values, dval, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        KC_CUDA(cudaMemcpyAsync(defined, ddef, (size_t)n, cudaMemcpyDeviceToHost, st));
+    } else {
+        KC_CUDA(cudaMemcpyAsync(hint, dint, 16, cudaMemcpyDeviceToHost, st));
+        if (topk)
+            KC_CUDA(cudaMemcpyAsync(topk, dint + 4, (size_t)k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    KC_CUDA(cudaStreamSynchronize(st));
+    if (!sum) {
+        if (t0)
+            *t0 = hint[0];
+        if (count)
+            *count = hint[1];
+        if (status_out)
+            *status_out = hint[2];
+    }
+    return KOHLER_OK;
+}
+
+int kohler_cuda_mean_contrast(kohler_cuda_ctx* ctx, const uint64_t* sum, const uint64_t* card,
+                              int n, double* values, uint8_t* defined)
+{
+    if (!ctx || (n > 0 && (!sum || !card || !values || !defined)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    return host_select(ctx, sum, card, nullptr, nullptr, n, 1, values, defined, nullptr, nullptr,
+                       nullptr, nullptr);
+}
+
+int kohler_cuda_optimal_threshold(kohler_cuda_ctx* ctx, const double* values,
+                                  const uint8_t* defined, int n, int* t0)
+{
+    if (!ctx || !t0 || (n > 0 && (!values || !defined)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int st = 0, count = 0;
+    const int rc = host_select(ctx, nullptr, nullptr, values, defined, n, 1, nullptr, nullptr, t0,
+                               nullptr, &count, &st);
+    if (rc)
+        return rc;
+    return st ? KOHLER_NO_BOUNDARY : KOHLER_OK;
+}
+
+int kohler_cuda_top_k_local_maxima(kohler_cuda_ctx* ctx, const double* values,
+                                   const uint8_t* defined, int n, int k, int* out, int* count)
+{
+    if (!ctx || !count || (n > 0 && (!values || !defined)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    *count = 0;
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (!out)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int st = 0, t0 = -1;
+    const int rc =
+        host_select(ctx, nullptr, nullptr, values, defined, n, k, nullptr, nullptr, &t0, out, count, &st);
+    if (rc)
+        return rc;
+    return st ? KOHLER_NO_BOUNDARY : KOHLER_OK;
+}
+
+} // extern "C"

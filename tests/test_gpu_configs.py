@@ -1,0 +1,115 @@
+"""The five BASELINE.json configurations at FULL size on the GPU, checked
+against the reference library (oracle/_ref) where it finishes in seconds and
+through size-independent properties everywhere: the total-variation and
+quarter-square identities (proj/tests/test_support.hpp:70-102), curve
+invariants, determinism, and the no-boundary case."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1707_05062_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+K = 6
+
+
+def run_batch(ctx, x, k=K):
+    """x: (n, h, w) uint8 CUDA tensor -> dict of host numpy outputs."""
+    n, h, w = x.shape
+    out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
+           "cards": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
+           "values": torch.zeros((n, 256), dtype=torch.float64, device="cuda"),
+           "defined": torch.zeros((n, 256), dtype=torch.uint8, device="cuda"),
+           "t0": torch.zeros(n, dtype=torch.int32, device="cuda"),
+           "topk": torch.zeros((n, k), dtype=torch.int32, device="cuda"),
+           "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda"),
+           "status": torch.zeros(n, dtype=torch.int32, device="cuda")}
+    ctx.analyze_batch_device(x, w, h, w, w * h, n, k, out)
+    torch.cuda.synchronize()
+    r = {key: v.cpu().numpy() for key, v in out.items()}
+    r["sums"] = r["sums"].view(np.uint64)
+    r["cards"] = r["cards"].view(np.uint64)
+    return r
+
+
+def identities(x, chunk=64):
+    """Per-image Σ|Δ| and Σ⌊Δ²/4⌋ over right and down pairs (torch, int64)."""
+    tv, qs = [], []
+    for s0 in range(0, x.shape[0], chunk):
+        a = x[s0:s0 + chunk].to(torch.int32)
+        t = torch.zeros(a.shape[0], dtype=torch.int64, device=x.device)
+        q = torch.zeros_like(t)
+        for d in ((a[:, :, 1:] - a[:, :, :-1]).abs(), (a[:, 1:, :] - a[:, :-1, :]).abs()):
+            t += d.sum(dim=(1, 2), dtype=torch.int64)
+            q += (d * d // 4).sum(dim=(1, 2), dtype=torch.int64)
+        tv.append(t)
+        qs.append(q)
+    return torch.cat(tv).cpu().numpy(), torch.cat(qs).cpu().numpy()
+
+
+def check_invariants(r, tv, qs):
+    s, c = r["sums"], r["cards"]
+    assert np.array_equal(c.sum(axis=1, dtype=np.uint64), tv.astype(np.uint64))
+    assert np.array_equal(s.sum(axis=1, dtype=np.uint64), qs.astype(np.uint64))
+    assert not c[:, 255].any()
+    assert np.all(s <= c * np.uint64(127))
+    assert np.all((c > 0) | (s == 0))
+    # double curve = IEEE division of the integers
+    with np.errstate(invalid="ignore", divide="ignore"):
+        v = np.where(c > 0, s.astype(np.float64) / np.maximum(c, 1).astype(np.float64), 0.0)
+    assert np.array_equal(r["values"], v)
+
+
+def check_against_reference(r, exp, idx=None):
+    idx = range(exp["sums"].shape[0]) if idx is None else idx
+    for j, i in enumerate(idx):
+        assert np.array_equal(r["sums"][i], exp["sums"][j]), i
+        assert np.array_equal(r["cards"][i], exp["cards"][j]), i
+        assert int(r["t0"][i]) == int(exp["t0"][j]), i
+        cnt = int(exp["topk_count"][j])
+        assert int(r["topk_count"][i]) == cnt
+        assert list(r["topk"][i, :cnt]) == list(exp["topk"][j, :cnt]), i
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_single_image_configs_vs_reference(ctx, ref, name):
+    x = synth.generate(name, device="cpu")
+    r = run_batch(ctx, x.cuda())
+    exp = ref.analyze_batch(x.numpy(), K, workers=8, threads=1)
+    check_against_reference(r, exp)
+    check_invariants(r, *identities(x.cuda()))
+    assert r["status"][0] == 0 and r["topk_count"][0] == K
+
+
+def test_c4_uniform_268mpx_vs_reference(ctx, ref):
+    x = synth.generate("C4", device="cpu")
+    r = run_batch(ctx, x.cuda())
+    import os
+    exp = ref.analyze_batch(x.numpy(), K, workers=os.cpu_count() or 8, threads=1)
+    check_against_reference(r, exp)
+    check_invariants(r, *identities(x.cuda()))
+
+
+def test_c3_video_batch(ctx, ref):
+    x = synth.generate("C3", device="cuda")
+    r = run_batch(ctx, x)
+    check_invariants(r, *identities(x, chunk=8))
+    sel = [0, 1, 255, 511]
+    exp = ref.analyze_batch(x[sel].cpu().numpy(), K, workers=1)
+    check_against_reference(r, exp, sel)
+    r2 = run_batch(ctx, x)
+    for key in r:
+        assert np.array_equal(r[key], r2[key])
+
+
+def test_c5_small_images_vs_reference(ctx, ref):
+    x = synth.generate("C5", device="cuda")
+    r = run_batch(ctx, x)
+    check_invariants(r, *identities(x, chunk=4096))
+    exp = ref.analyze_batch(x.cpu().numpy(), K, workers=1)
+    check_against_reference(r, exp)
+    fam_b = np.arange(x.shape[0]) % 4 == 1
+    assert np.all(r["status"][fam_b] == 1) and np.all(r["t0"][fam_b] == -1)
+    assert not r["cards"][fam_b].any()
+    assert np.all(r["status"][~fam_b] == 0)
