@@ -96,11 +96,18 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout=3.0):
+        """Block until nvidia-smi has produced its first sample."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.mark = len(self.lines)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
-        time.sleep(0.05)
+        time.sleep(0.06)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -279,7 +286,7 @@ def main():
     torch.cuda.synchronize()
 
     sampler = ClockSampler(dev.index if world == 1 else local).start()
-    time.sleep(0.1)
+    sampler.wait_first()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

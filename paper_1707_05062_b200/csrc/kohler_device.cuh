@@ -12,7 +12,7 @@
 // has second difference +1 at lo+1 and hi+1 and -1 at floor(s/2)+1 and
 // ceil(s/2)+1, and equal pairs cancel exactly.  `corr` holds the border
 // terms (missing neighbours) and the compensation for the equal "fake" pairs
-// the universal lane path creates at row ends (see process_step()).
+// the universal lane path creates at row ends (see border_terms()).
 //
 // Histogram layout in shared memory (128 KiB, "lane-striped"): 512 rows of
 // 256 bytes; word (row, half, lane) lives at row*256 + half*128 + lane*4, so
@@ -82,9 +82,18 @@ __device__ __forceinline__ void accumulate_segment(unsigned char* sm, const uint
     }
 }
 
-__device__ __forceinline__ uint32_t byte_of(const uint32_t (&c)[4], int i)
+// Byte i (compile-time index after unrolling) of a 16-byte segment.
+__device__ __forceinline__ uint32_t byte_at(const uint32_t (&c)[4], int i)
 {
     return (c[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+}
+
+// Byte e (runtime index, 0..15) without dynamic register indexing (which
+// would force the segment into local memory).
+__device__ __forceinline__ uint32_t byte_dyn(const uint32_t (&c)[4], int e)
+{
+    const uint32_t wd = e < 4 ? c[0] : e < 8 ? c[1] : e < 12 ? c[2] : c[3];
+    return (wd >> (8 * (e & 3))) & 0xFFu;
 }
 
 // Replace bytes i > e of the segment by v (row-end lanes).
@@ -150,29 +159,41 @@ struct StepGeom {
 // Band-first row: +1 per real pixel (its up pair belongs to the row above /
 // does not exist).  Row start: +1 (no left pair).  Halo row pixels (row r1 of
 // a band with r1 < h): -1 each (their up pair is owned, P gains 1).
-__device__ __forceinline__ void border_terms(int* corr, const StepGeom& g, uint32_t (&c)[4],
-                                             uint32_t (&n)[4], uint32_t& rn, bool has_down)
+// `corr` is lane-striped like the histograms (word (v, lane) at
+// v*128 + lane*4, 32 KiB) so its updates are bank-conflict free, and the
+// per-pixel loops are branch-free (a disabled term adds 0).
+__device__ __forceinline__ void corr_add(unsigned char* corr, uint32_t lane4, uint32_t v, int d)
+{
+    atomicAdd(reinterpret_cast<int*>(corr + (v << 7) + lane4), d);
+}
+
+__device__ __forceinline__ void border_terms(unsigned char* corr, uint32_t lane4, const StepGeom& g,
+                                             uint32_t (&c)[4], uint32_t (&n)[4], uint32_t& rn,
+                                             bool has_down)
 {
     const int e = g.w - 1 - g.x0;  // index of the last real pixel if < 16
-    const int last = e < 15 ? e : 15;
     if (g.x0 == 0)
-        atomicAdd(&corr[c[0] & 0xFFu], 1);
-    if (g.y == 0)
-        for (int i = 0; i <= last; ++i)
-            atomicAdd(&corr[byte_of(c, i)], 1);
-    if (!has_down)
-        for (int i = 0; i <= last; ++i)
-            atomicAdd(&corr[byte_of(c, i)], -1);
-    else if (g.y + 1 == g.band_rows)
-        for (int i = 0; i <= last; ++i)
-            atomicAdd(&corr[byte_of(n, i)], -1);
+        corr_add(corr, lane4, c[0] & 0xFFu, 1);
+    // +1 (band-first row: no owned up pair), -1 (last image row: missing down
+    // pair +1, fake equal down pair -2); both at once cancel.
+    const int dcur = (g.y == 0 ? 1 : 0) - (has_down ? 0 : 1);
+    if (dcur != 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            corr_add(corr, lane4, byte_at(c, i), i <= e ? dcur : 0);
+    }
+    if (has_down && g.y + 1 == g.band_rows) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            corr_add(corr, lane4, byte_at(n, i), i <= e ? -1 : 0);
+    }
     if (e <= 15) {
-        const uint32_t v = byte_of(c, e);
+        const uint32_t v = byte_dyn(c, e);
         fill_tail(c, e, v);
         if (has_down)
             fill_tail(n, e, v);
         rn = v;
-        atomicAdd(&corr[v], -1);
+        corr_add(corr, lane4, v, -1);
     }
     if (!has_down) {
 #pragma unroll
@@ -333,24 +354,53 @@ __device__ int warp_select(const double* val, const uint8_t* def, int n, int k,
     }
     __syncwarp();
 
-    int cnt = 0;
-    for (int i0 = 0; i0 < nm; i0 += 32) {
-        const int i = i0 + lane;
-        bool sel = false;
-        int ti = 0;
-        if (i < nm) {
-            const double v = s.mv[i];
-            ti = s.mt[i];
-            int rank = 0;
-            for (int j = 0; j < nm && rank < k; ++j) {
-                const double u = s.mv[j];
-                rank += (u > v) || (u == v && s.mt[j] < ti);
+    // Top-k by k rounds of a warp argmax over the unselected maxima
+    // (value desc, t asc), then emit the selected ones in t order (the maxima
+    // array is already sorted by t).  Lane L owns maxima L, L+32, ... and
+    // tracks them in a 64-bit mask (nm <= n/2+1 <= 2049 for n <= 4096).
+    unsigned long long selmask = 0ull;
+    const int rounds = k < nm ? k : nm;
+    if (rounds == nm) {
+        selmask = ~0ull;
+    } else {
+        for (int r = 0; r < rounds; ++r) {
+            double lv = 0.0;
+            int lbt = -1, lj = -1;
+            for (int j = 0, i = lane; i < nm; ++j, i += 32) {
+                if ((selmask >> j) & 1ull)
+                    continue;
+                const double v = s.mv[i];
+                const int t = s.mt[i];
+                if (lbt < 0 || v > lv || (v == lv && t < lbt)) {
+                    lv = v;
+                    lbt = t;
+                    lj = j;
+                }
             }
-            sel = rank < k;
+            double bvv = lv;
+            int btt = lbt, bl = lane;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xFFFFFFFFu, bvv, off);
+                const int ot = __shfl_xor_sync(0xFFFFFFFFu, btt, off);
+                const int ol = __shfl_xor_sync(0xFFFFFFFFu, bl, off);
+                if (ot >= 0 && (btt < 0 || ov > bvv || (ov == bvv && ot < btt))) {
+                    bvv = ov;
+                    btt = ot;
+                    bl = ol;
+                }
+            }
+            if (lane == bl && lj >= 0)
+                selmask |= 1ull << lj;
         }
+    }
+    int cnt = 0;
+    for (int j = 0, i0 = 0; i0 < nm; ++j, i0 += 32) {
+        const int i = i0 + lane;
+        const bool sel = i < nm && ((selmask >> j) & 1ull);
         const unsigned sb = __ballot_sync(0xFFFFFFFFu, sel);
         if (sel && out_topk)
-            out_topk[cnt + __popc(sb & lt)] = ti;
+            out_topk[cnt + __popc(sb & lt)] = s.mt[i];
         cnt += __popc(sb);
     }
     if (lane == 0) {
@@ -360,6 +410,159 @@ __device__ int warp_select(const double* val, const uint8_t* def, int n, int k,
             *out_count = cnt;
     }
     return 0;
+}
+
+// Block-parallel selection for 256-level curves: 256 threads, thread t owns
+// threshold t.  Same rules as warp_select (proj/src/threshold.cpp:25-82), but
+// every step is a block-wide scan/reduction instead of one warp's serial loop,
+// which keeps the per-image tail short.  `val`/`def` are in shared memory;
+// `scr` needs 256*(8+4) + 64 bytes.  Must be called by all 256 threads of a
+// group of 8 warps that can barrier with bar.sync `bar_id` (256 threads).
+// Returns (to every thread) 1 for no boundary, else 0.
+__device__ __forceinline__ void bar256(int id)
+{
+    asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
+
+__device__ int block_select256(const double* val, const uint8_t* def, int k, unsigned char* scr,
+                               int bar_id, int* out_t0, int* out_topk, int* out_count)
+{
+    const int t = threadIdx.x & 255;
+    const int lane = t & 31, wp = t >> 5;
+    const unsigned lt = lanemask_lt();
+    double* mv = reinterpret_cast<double*>(scr);             // [256] maxima values
+    int* mt = reinterpret_cast<int*>(scr + 2048);            // [256] maxima t
+    int* wsum = reinterpret_cast<int*>(scr + 3072);          // [8]
+    int* wmax = wsum + 8;                                    // [8]
+    int* wmin = wmax + 8;                                    // [8]
+    double* wbv = reinterpret_cast<double*>(scr + 3072 + 96); // [8]
+    int* wbt = reinterpret_cast<int*>(scr + 3072 + 160);     // [8]
+
+    const bool d = def[t] != 0;
+    const double v = val[t];
+
+    // argmax with ties to the smallest t
+    double bv = v;
+    int bt = d ? t : -1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, off);
+        const int ot = __shfl_xor_sync(0xFFFFFFFFu, bt, off);
+        if (ot >= 0 && (bt < 0 || ov > bv || (ov == bv && ot < bt))) {
+            bv = ov;
+            bt = ot;
+        }
+    }
+    // previous defined index (max-scan of d ? t : -1), inclusive then shift
+    int pd = d ? t : -1;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xFFFFFFFFu, pd, off);
+        if (lane >= off && o > pd)
+            pd = o;
+    }
+    if (lane == 31) {
+        wmax[wp] = pd;
+        wbv[wp] = bv;
+        wbt[wp] = bt;
+    }
+    bar256(bar_id);
+    int carry = -1;
+    for (int i = 0; i < wp; ++i)
+        carry = wmax[i] > carry ? wmax[i] : carry;
+    const int pd_incl = pd > carry ? pd : carry;
+    int prev = __shfl_up_sync(0xFFFFFFFFu, pd_incl, 1);
+    if (lane == 0)
+        prev = carry;
+    // prev = last defined index < t (or -1)
+    const bool start = d && (prev < 0 || val[prev] != v);
+    // next run start after t: suffix min-scan of (start ? t : 256)
+    int ns = start ? t : 256;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_down_sync(0xFFFFFFFFu, ns, off);
+        if (lane + off < 32 && o < ns)
+            ns = o;
+    }
+    if (lane == 0)
+        wmin[wp] = ns;
+    // block argmax result
+    double gbv = 0.0;
+    int gbt = -1;
+    for (int i = 0; i < 8; ++i) {
+        const double ov = wbv[i];
+        const int ot = wbt[i];
+        if (ot >= 0 && (gbt < 0 || ov > gbv || (ov == gbv && ot < gbt))) {
+            gbv = ov;
+            gbt = ot;
+        }
+    }
+    bar256(bar_id);
+    int carry_n = 256;
+    for (int i = wp + 1; i < 8; ++i)
+        carry_n = wmin[i] < carry_n ? wmin[i] : carry_n;
+    const int ns_incl = ns < carry_n ? ns : carry_n;
+    int nxt = __shfl_down_sync(0xFFFFFFFFu, ns_incl, 1);
+    if (lane == 31)
+        nxt = carry_n;
+    // nxt = first run start > t (or 256)
+    const bool is_max = start && (prev < 0 || v > val[prev]) && (nxt >= 256 || v > val[nxt]);
+    // any run at all? (a defined entry exists iff the argmax exists)
+    const bool any = gbt >= 0;
+
+    // compact maxima in t order
+    const unsigned mb = __ballot_sync(0xFFFFFFFFu, is_max);
+    if (lane == 0)
+        wsum[wp] = __popc(mb);
+    bar256(bar_id);
+    int base = 0, nm = 0;
+    for (int i = 0; i < 8; ++i) {
+        base += i < wp ? wsum[i] : 0;
+        nm += wsum[i];
+    }
+    const int pos = base + __popc(mb & lt);
+    if (is_max) {
+        mv[pos] = v;
+        mt[pos] = t;
+    }
+    bar256(bar_id);
+    // rank by (value desc, t asc); keep rank < k
+    bool sel = false;
+    if (is_max) {
+        if (k >= nm) {
+            sel = true;
+        } else {
+            // independent loads, 8 per trip (mv/mt are padded to 256)
+            int rank = 0;
+            for (int j0 = 0; j0 < nm && rank < k; j0 += 8) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int j = j0 + q;
+                    const double u = mv[j];
+                    rank += (j < nm) && ((u > v) || (u == v && mt[j] < t));
+                }
+            }
+            sel = rank < k;
+        }
+    }
+    const unsigned sb = __ballot_sync(0xFFFFFFFFu, sel);
+    if (lane == 0)
+        wsum[8 + wp] = __popc(sb);  // wmax area is free now
+    bar256(bar_id);
+    int sbase = 0, cnt = 0;
+    for (int i = 0; i < 8; ++i) {
+        sbase += i < wp ? wsum[8 + i] : 0;
+        cnt += wsum[8 + i];
+    }
+    if (sel && out_topk)
+        out_topk[sbase + __popc(sb & lt)] = t;
+    if (t == 0) {
+        if (out_t0)
+            *out_t0 = any ? gbt : -1;
+        if (out_count)
+            *out_count = any ? cnt : 0;
+    }
+    return any ? 0 : 1;
 }
 
 } // namespace kohler_dev

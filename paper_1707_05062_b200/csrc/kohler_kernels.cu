@@ -32,7 +32,6 @@ using namespace kohler_dev;
 namespace {
 
 constexpr int kWideThreads = 1024;
-constexpr int kWideWarps = kWideThreads / 32;
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
 constexpr int kMaxSelectLevels = 4096;
 
@@ -51,6 +50,9 @@ struct WideParams {
     unsigned long long* acc;  // [n][copies][512]
     int copies;
     unsigned* tickets;  // [n]
+    unsigned long long seg_magic;  // floor(2^64 / nseg) + 1 (nseg > 1)
+    int adv_q, adv_r;              // 32 = adv_q * nseg + adv_r (one unit)
+    long long cta_q, cta_r;        // U = cta_q * G + cta_r (CTA range sizes)
     int k;
     int select;
     uint64_t* sums;
@@ -64,8 +66,8 @@ struct WideParams {
 };
 
 // Shared-memory map of K1 (dynamic).
-constexpr uint32_t kSmCorr = kStripedBytes;                 // int[256]
-constexpr uint32_t kSmCorrCopy = kSmCorr + 1024;            // int[256]
+constexpr uint32_t kSmCorr = kStripedBytes;                 // int[256][32] lane-striped
+constexpr uint32_t kSmCorrCopy = kSmCorr + 32768;           // int[256]
 constexpr uint32_t kSmTot = kSmCorrCopy + 1024;             // u64[1024]
 constexpr uint32_t kSmVal = kSmTot + 8192;                  // i64[512]
 constexpr uint32_t kSmCurve = kSmVal + 4096;                // u64 sum[256], card[256]
@@ -74,10 +76,41 @@ constexpr uint32_t kSmDef = kSmMean + 2048;                 // u8[256]
 constexpr uint32_t kSmScratch = kSmDef + 256;               // rv,rt,mv,mt [256]
 constexpr uint32_t kSmWideBytes = kSmScratch + 256 * (8 + 4 + 8 + 4);
 
-__device__ __forceinline__ long long cta_of_unit(long long u, long long G, long long U)
+// CTA owning unit u under the balanced partition (first cta_r CTAs hold
+// cta_q + 1 units, the rest cta_q).
+__device__ __forceinline__ long long cta_of_unit(long long u, long long q, long long r)
 {
-    return ((u + 1) * G - 1) / U;
+    const long long big = r * (q + 1);
+    return u < big ? u / (q + 1) : r + (u - big) / q;
 }
+
+// Programmatic dependent launch (sm_90+): a step's prologue and main loop may
+// run while the previous step's tail finishes; everything that touches the
+// shared workspace or the outputs waits for the previous grid first.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+#ifdef KOHLER_PHASES
+// Debug builds only (tools/phase_probe.cu): per-CTA globaltimer stamps.
+__device__ unsigned long long g_phase[2048][8];
+__device__ unsigned g_smid[2048];
+__device__ int g_rot;
+__device__ __forceinline__ void phase(int i)
+{
+    if (threadIdx.x == 0 && blockIdx.x < 2048) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_phase[blockIdx.x][i] = t;
+        if (i == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_smid[blockIdx.x] = sm;
+        }
+    }
+}
+#else
+__device__ __forceinline__ void phase(int) {}
+#endif
 
 // Last CTA of an image: sum accumulator copies, reset them, rebuild the
 // curve, write it, and (optionally) select.
@@ -91,17 +124,24 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
     uint8_t* def = sm + kSmDef;
 
     if (tid < 512) {
-        unsigned long long* a = p.acc + (size_t)img * p.copies * 512;
+        unsigned long long* a = p.acc + (size_t)img * p.copies * 512 + tid;
+        unsigned long long v[kAccCopiesSingle];
+#pragma unroll
+        for (int c = 0; c < kAccCopiesSingle; ++c)
+            v[c] = c < p.copies ? __ldcg(a + c * 512) : 0ull;
         unsigned long long s = 0;
-        for (int c = 0; c < p.copies; ++c) {
-            s += __ldcg(a + c * 512 + tid);
-            __stcg(a + c * 512 + tid, 0ull);
+#pragma unroll
+        for (int c = 0; c < kAccCopiesSingle; ++c) {
+            s += v[c];
+            if (c < p.copies)
+                __stcg(a + c * 512, 0ull);
         }
         sval[tid] = (long long)s;
     }
     if (tid == 0)
         p.tickets[img] = 0;
     __syncthreads();
+    phase(4);
     const int warp = tid >> 5;
     long long* tmp = reinterpret_cast<long long*>(sm + kSmTot);  // reuse
     if (warp == 0)
@@ -127,25 +167,23 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
             p.defined[(size_t)img * 256 + tid] = cc ? 1 : 0;
     }
     __syncthreads();
-    if (p.select && warp == 0) {
-        unsigned char* scr = sm + kSmScratch;
-        SelectScratch s{reinterpret_cast<double*>(scr), reinterpret_cast<int*>(scr + 2048),
-                        reinterpret_cast<double*>(scr + 3072), reinterpret_cast<int*>(scr + 5120)};
-        const int st = warp_select(mean, def, 256, p.k, s, p.t0s ? p.t0s + img : nullptr,
-                                   p.topks ? p.topks + (size_t)img * p.k : nullptr,
-                                   p.topk_counts ? p.topk_counts + img : nullptr);
+    phase(5);
+    if (p.select && tid < 256) {
+        const int st = block_select256(mean, def, p.k, sm + kSmScratch, 1,
+                                       p.t0s ? p.t0s + img : nullptr,
+                                       p.topks ? p.topks + (size_t)img * p.k : nullptr,
+                                       p.topk_counts ? p.topk_counts + img : nullptr);
         if (tid == 0 && p.status)
             p.status[img] = st;
     }
+    phase(6);
 }
 
 // CTA flush of one image's partial: reduce the striped histogram (zeroing it
 // for the next image), form the 512 combinations, REDG them, take a ticket.
-__device__ void flush_image(const WideParams& p, int img, unsigned char* sm, long long G,
-                            long long U)
+__device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
 {
     const int tid = threadIdx.x;
-    int* corr = reinterpret_cast<int*>(sm + kSmCorr);
     int* corr_copy = reinterpret_cast<int*>(sm + kSmCorrCopy);
     unsigned long long* tot = reinterpret_cast<unsigned long long*>(sm + kSmTot);
 
@@ -153,21 +191,37 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, lon
         // thread t owns (row t>>1, half t&1): 32 lane words, read rotated
         // by t&7 so a warp's LDS.128 hit distinct bank quads.
         uint4* row = reinterpret_cast<uint4*>(sm + (tid >> 1) * 256 + (tid & 1) * 128);
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            v[j] = row[(j + tid) & 7];
         unsigned long long s = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int q = (j + tid) & 7;
-            const uint4 v = row[q];
-            s += (unsigned long long)v.x + v.y + v.z + v.w;
-            row[q] = make_uint4(0, 0, 0, 0);
+            s += (unsigned long long)v[j].x + v[j].y + v[j].z + v[j].w;
+            row[(j + tid) & 7] = make_uint4(0, 0, 0, 0);
         }
         tot[tid] = s;
         if (tid < 256) {
-            corr_copy[tid] = corr[tid];
-            corr[tid] = 0;
+            // corr row tid: 32 lane words, same rotation
+            int4* cr = reinterpret_cast<int4*>(sm + kSmCorr + tid * 128);
+            int4 q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                q[j] = cr[(j + tid) & 7];
+            int cs = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                cs += q[j].x + q[j].y + q[j].z + q[j].w;
+                cr[(j + tid) & 7] = make_int4(0, 0, 0, 0);
+            }
+            corr_copy[tid] = cs;
         }
     }
     __syncthreads();
+    // the workspace (acc, tickets, chunk counters) and outputs may still be in
+    // use by the previous launch in this stream
+    pdl_wait();
     if (tid < 512) {
         const long long v = combo(
             tid, [&](int x) { return tot[2 * x + 1]; },
@@ -183,18 +237,100 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, lon
     __syncthreads();
     __shared__ int s_last;
     if (tid == 0) {
-        const long long first = cta_of_unit((long long)img * p.upi, G, U);
-        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, G, U);
+        const long long first = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
+        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, p.cta_q, p.cta_r);
         const unsigned expected = (unsigned)(last - first + 1);
         const unsigned prev = atomicAdd(p.tickets + img, 1u);
         s_last = (prev + 1 == expected);
     }
     __syncthreads();
+    phase(3);
     if (s_last) {
         __threadfence();
         finish_image(p, img, sm);
     }
     __syncthreads();
+}
+
+// A lane's 16-pixel segment: unit u covers flattened (row, segment) indices
+// [32u, 32u + 32) of an image band; lane L takes 32u + L.  Cursor walks a
+// warp's contiguous unit range without divisions.
+struct Cursor {
+    int y;    // band-relative row
+    int seg;  // segment in the row
+    // advance by one unit = 32 segments = adv_q rows + adv_r segments
+    __device__ __forceinline__ void advance(int nseg, int adv_q, int adv_r)
+    {
+        seg += adv_r;
+        y += adv_q;
+        if (seg >= nseg) {
+            seg -= nseg;
+            ++y;
+        }
+    }
+};
+
+struct Segment {
+    uint32_t c[4];
+    uint32_t n[4];
+    uint32_t rn;
+};
+
+// Loads of one lane's segment at band-relative (y, seg): the row, the row
+// below (when the pair exists) and the right-neighbour byte (when inside the
+// row).  No shuffles: every load is issued a unit ahead of its use.
+template <bool VEC>
+__device__ __forceinline__ void fetch(const WideParams& p, const uint8_t* base, int y, int seg,
+                                      Segment& s)
+{
+    const int x0 = seg << 4;
+    const uint8_t* row = base + (size_t)y * p.pitch;
+    if (y < p.band_rows) {
+        load_segment<VEC>(row, x0, p.w, s.c);
+        if (p.r0 + y + 1 < p.h_total)
+            load_segment<VEC>(row + p.pitch, x0, p.w, s.n);
+        if (x0 + 16 < p.w)
+            s.rn = __ldg(row + x0 + 16);
+    }
+}
+
+__device__ __forceinline__ void zero_hist(unsigned char* sm, int tid)
+{
+    uint4* z = reinterpret_cast<uint4*>(sm);
+    for (int i = tid; i < (int)(kStripedBytes / 16); i += kWideThreads)
+        z[i] = make_uint4(0, 0, 0, 0);
+    uint4* zc = reinterpret_cast<uint4*>(sm + kSmCorr);
+    for (int i = tid; i < 32768 / 16; i += kWideThreads)
+        zc[i] = make_uint4(0, 0, 0, 0);
+}
+
+// Accumulate one lane's segment.  Warp-uniform fast path when every lane is
+// interior (no border terms); otherwise each border lane fixes itself up.
+__device__ __forceinline__ void process(const WideParams& p, unsigned char* sm, int y, int seg,
+                                        uint32_t lane4, Segment& s)
+{
+    const int x0 = seg << 4;
+    const bool active = y < p.band_rows;
+    const bool interior = active && x0 != 0 && x0 + 16 < p.w && y != 0 && y + 1 < p.band_rows;
+    if (!__all_sync(0xFFFFFFFFu, interior)) {
+        if (active && !interior) {
+            const int gy = p.r0 + y;
+            StepGeom geom{p.w, y, p.band_rows, gy, p.h_total, x0};
+            border_terms(sm + kSmCorr, lane4, geom, s.c, s.n, s.rn,
+                         gy + 1 < p.h_total);
+        }
+        if (!active)
+            return;
+    }
+    accumulate_segment(sm, s.c, s.n, s.rn, lane4);
+}
+
+__device__ __forceinline__ void unit_pos(const WideParams& p, long long u, int lane, int& y, int& seg)
+{
+    const unsigned long long g = (unsigned long long)u * 32ull + (unsigned)lane;
+    const unsigned long long q = p.nseg == 1 ? g : __umul64hi(g, p.seg_magic);
+    y = (int)q;
+    seg = (int)(g - q * (unsigned long long)p.nseg);
 }
 
 template <bool VEC>
@@ -203,87 +339,79 @@ __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams 
     extern __shared__ __align__(16) unsigned char sm[];
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int warp = tid >> 5;
     const uint32_t lane4 = (uint32_t)lane * 4u;
-    int* corr = reinterpret_cast<int*>(sm + kSmCorr);
+    phase(0);
 
-    {
-        uint4* z = reinterpret_cast<uint4*>(sm);
-        for (int i = tid; i < (int)(kStripedBytes / 16); i += kWideThreads)
-            z[i] = make_uint4(0, 0, 0, 0);
-        if (tid < 256)
-            corr[tid] = 0;
-    }
-    __syncthreads();
+#ifdef KOHLER_PHASES
+    const long long rb = (blockIdx.x + g_rot) % gridDim.x;  // debug: rotate ranges vs CTAs
+#else
+    const long long rb = blockIdx.x;
+#endif
+    // balanced partition: the first cta_r ranges hold cta_q + 1 units
+    const long long cs = rb * p.cta_q + (rb < p.cta_r ? rb : p.cta_r);
+    const long long ce = cs + p.cta_q + (rb < p.cta_r ? 1 : 0);
 
-    const long long U = p.total_units;
-    const long long G = gridDim.x;
-    const long long cs = U * blockIdx.x / G;
-    const long long ce = U * (blockIdx.x + 1) / G;
-    if (cs >= ce)
-        return;
-    const int i_first = (int)(cs / p.upi);
-    const int i_last = (int)((ce - 1) / p.upi);
-    const long long nseg_img = (long long)p.band_rows * p.nseg;
-    const int nseg = p.nseg;
-    const int w = p.w;
-
-    for (int img = i_first; img <= i_last; ++img) {
-        const long long ibase = (long long)img * p.upi;
-        const long long a = cs > ibase ? cs : ibase;
-        const long long b = ce < ibase + p.upi ? ce : ibase + p.upi;
-        const long long len = b - a;
-        const long long wa = a + len * warp / kWideWarps;
-        const long long wb = a + len * (warp + 1) / kWideWarps;
-        const uint8_t* base = p.px + (size_t)img * p.image_stride;
-
-        if (wa < wb) {
-            long long g = (wa - ibase) * 32 + lane;
-            int y = (int)(g / nseg);
-            int seg = (int)(g - (long long)y * nseg);
-            for (long long u = wa; u < wb; ++u) {
-                const bool active = g < nseg_img;
-                const int x0 = seg * 16;
-                const uint8_t* row = base + (size_t)y * p.pitch;
-                const int gy = p.r0 + y;
-                const bool has_down = gy + 1 < p.h_total;
-                uint32_t c[4] = {0, 0, 0, 0}, nx[4] = {0, 0, 0, 0};
-                uint32_t rn = 0;
-                if (active) {
-                    load_segment<VEC>(row, x0, w, c);
-                    if (has_down)
-                        load_segment<VEC>(row + p.pitch, x0, w, nx);
-                    if (lane == 31 && x0 + 16 < w)
-                        rn = __ldg(row + x0 + 16);
-                }
-                const uint32_t sh = __shfl_down_sync(0xFFFFFFFFu, c[0] & 0xFFu, 1);
-                if (lane < 31)
-                    rn = sh;
-                if (active) {
-                    const bool interior = (x0 != 0) && (x0 + 16 < w) && has_down && (y != 0) &&
-                                          (y + 1 != p.band_rows);
-                    if (!interior) {
-                        StepGeom geom{w, y, p.band_rows, gy, p.h_total, x0};
-                        border_terms(corr, geom, c, nx, rn, has_down);
-                    }
-                    accumulate_segment(sm, c, nx, rn, lane4);
-                }
-                g += 32;
-                seg += 32;
-                if (seg >= nseg) {
-                    if (nseg >= 32) {
-                        seg -= nseg;
-                        ++y;
-                    } else {
-                        y += seg / nseg;
-                        seg %= nseg;
-                    }
-                }
-            }
+    bool zeroed = false;
+    bool flushed = false;
+    if (cs < ce) {
+        int i_first = 0, i_last = 0;
+        if (p.n > 1) {
+            i_first = (int)(cs / p.upi);
+            i_last = (int)((ce - 1) / p.upi);
         }
-        __syncthreads();
-        flush_image(p, img, sm, G, U);
+        for (int img = i_first; img <= i_last; ++img) {
+            const long long ibase = (long long)img * p.upi;
+            const long long a = (cs > ibase ? cs : ibase) - ibase;
+            const long long b = (ce < ibase + p.upi ? ce : ibase + p.upi) - ibase;
+            const uint8_t* base = p.px + (size_t)img * p.image_stride;
+            // warp w walks a contiguous run of the CTA's sub-range [a, b),
+            // ping-ponging two register buffers one unit ahead
+            const int warp = tid >> 5;
+            const long long u0 = a + (b - a) * warp / 32;
+            int rem = (int)(a + (b - a) * (warp + 1) / 32 - u0);
+            const int aq = p.adv_q, ar = p.adv_r;
+            Cursor c0, c1;
+            unit_pos(p, u0, lane, c0.y, c0.seg);
+            Segment A, B;
+            A.rn = B.rn = 0;
+            if (rem > 0)
+                fetch<VEC>(p, base, c0.y, c0.seg, A);
+            if (!zeroed) {
+                // overlap the first loads with clearing the histogram
+                zero_hist(sm, tid);
+                __syncthreads();
+                zeroed = true;
+                phase(1);
+            }
+            c1 = c0;
+            c1.advance(p.nseg, aq, ar);
+            while (rem > 0) {
+                if (rem > 1)
+                    fetch<VEC>(p, base, c1.y, c1.seg, B);
+                process(p, sm, c0.y, c0.seg, lane4, A);
+                if (--rem == 0)
+                    break;
+                c0 = c1;
+                c0.advance(p.nseg, aq, ar);
+                if (rem > 1)
+                    fetch<VEC>(p, base, c0.y, c0.seg, A);
+                process(p, sm, c1.y, c1.seg, lane4, B);
+                --rem;
+                c1 = c0;
+                c1.advance(p.nseg, aq, ar);
+            }
+            __syncthreads();
+            if (img == i_last) {
+                phase(2);
+                pdl_trigger();  // the next launch may start as SMs free up
+            }
+            flush_image(p, img, sm);
+            flushed = true;
+        }
     }
+    if (!flushed)
+        pdl_trigger();
+    phase(7);
 }
 
 // Definition-level oracle kernel: block t scans every
@@ -511,8 +639,10 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     const long long segs = (long long)band_rows * nseg;
     const long long upi = (segs + 31) / 32;
     const long long U = upi * n;
+    // One CTA per SM, leaving one SM free: with programmatic dependent launch
+    // the next launch's CTAs then never wait for this launch's serial tail.
     long long G = (U + 63) / 64;
-    G = std::max(1ll, std::min<long long>(G, ctx->sm_count));
+    G = std::max(1ll, std::min<long long>(G, std::max(1, ctx->sm_count - 1)));
     const int copies = n == 1 ? kAccCopiesSingle : 1;
     int rc = ctx->acc.ensure((size_t)n * copies * 512 * sizeof(unsigned long long), true);
     if (rc)
@@ -536,6 +666,12 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     p.acc = static_cast<unsigned long long*>(ctx->acc.p);
     p.copies = copies;
     p.tickets = static_cast<unsigned*>(ctx->tickets.p);
+    p.adv_q = 32 / nseg;
+    p.adv_r = 32 % nseg;
+    p.cta_q = U / G;
+    p.cta_r = U % G;
+    p.seg_magic = nseg > 1 ? (unsigned long long)((((unsigned __int128)1) << 64) / (unsigned)nseg) + 1ull
+                           : 0ull;
     p.k = k;
     p.select = select;
     p.sums = o.sums;
@@ -557,10 +693,20 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         ctx->wide_attr_set = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kWideThreads);
+    cfg.dynamicSmemBytes = kSmWideBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (vec)
-        wide_kernel<true><<<(unsigned)G, kWideThreads, kSmWideBytes, stream>>>(p);
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true>, p));
     else
-        wide_kernel<false><<<(unsigned)G, kWideThreads, kSmWideBytes, stream>>>(p);
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false>, p));
     KC_CUDA(cudaGetLastError());
     ctx->last_launches += 1;
     return KOHLER_OK;

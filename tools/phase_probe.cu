@@ -1,0 +1,96 @@
+// Phase probe (debug only): builds kohler_kernels.cu with KOHLER_PHASES and
+// prints per-CTA globaltimer phase durations of the fused launch on a
+// C2-sized image: [0] start -> [1] histogram zeroed (first loads in flight)
+// -> [2] main loop done -> [3] CTA exit (flush, and for the last CTA the
+// reconstruction + selection).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DKOHLER_PHASES \
+//        -Iinclude -o tools/phase_probe tools/phase_probe.cu
+#include "../paper_1707_05062_b200/csrc/kohler_kernels.cu"
+
+#include <algorithm>
+#include <vector>
+
+int main(int argc, char** argv)
+{
+    const int w = argc > 1 ? atoi(argv[1]) : 5184, h = argc > 2 ? atoi(argv[2]) : 3456;
+    const int reps = 20;
+    if (argc > 3) { int rot = atoi(argv[3]); cudaMemcpyToSymbol(g_rot, &rot, sizeof(int)); }
+    kohler_cuda_ctx* ctx = nullptr;
+    if (kohler_cuda_create(0, &ctx)) { printf("create: %s\n", kohler_cuda_last_error()); return 1; }
+    size_t pitch = (w + 127) / 128 * 128;
+    std::vector<uint8_t> img(pitch * h);
+    uint32_t x = 12345;
+    for (int y = 0; y < h; ++y)
+        for (int i = 0; i < w; ++i) {
+            x = x * 1664525u + 1013904223u;
+            int v = (i * 200 / w + y * 200 / h) / 2 + (int)((x >> 24) % 11) - 5;
+            img[(size_t)y * pitch + i] = (uint8_t)std::min(255, std::max(0, v));
+        }
+    const int copies = 12;
+    uint8_t* d; cudaMalloc(&d, pitch * h * copies);
+    for (int c = 0; c < copies; ++c) cudaMemcpy(d + c * pitch * h, img.data(), pitch * h, cudaMemcpyHostToDevice);
+    uint64_t* out; cudaMalloc(&out, 8192);
+    int* ints; cudaMalloc(&ints, 256);
+    cudaStream_t st; cudaStreamCreate(&st);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int r = 0; r < 5; ++r)
+        kohler_cuda_analyze_batch_device(ctx, d + (r % copies) * pitch * h, 1, w, h, pitch, pitch * h, 6, out, out + 256, nullptr, nullptr, ints, ints + 8, ints + 1, ints + 2, st);
+    cudaStreamSynchronize(st);
+    cudaEventRecord(a, st);
+    for (int r = 0; r < 200; ++r)
+        kohler_cuda_analyze_batch_device(ctx, d + (r % copies) * pitch * h, 1, w, h, pitch, pitch * h, 6, out, out + 256, nullptr, nullptr, ints, ints + 8, ints + 1, ints + 2, st);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("pipelined (PDL) back-to-back: %.2f us/step\n", ms * 1000 / 200);
+    std::vector<double> tot;
+    for (int r = 0; r < reps; ++r) {
+        cudaStreamSynchronize(st);
+        cudaEventRecord(a, st);
+        kohler_cuda_analyze_batch_device(ctx, d + (r % copies) * pitch * h, 1, w, h, pitch, pitch * h, 6, out, out + 256, nullptr, nullptr, ints, ints + 8, ints + 1, ints + 2, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        tot.push_back(ms * 1000);
+    }
+    std::sort(tot.begin(), tot.end());
+    printf("isolated launch (event): median %.2f us\n", tot[reps / 2]);
+    static unsigned long long ph[2048][8];
+    cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
+    const long long U = ((long long)h * ((w + 15) / 16) + 31) / 32;
+    int G = (int)std::max(1ll, std::min<long long>((U + 63) / 64, ctx->sm_count - 1));
+    printf("grid %d CTAs\n", G);
+    unsigned long long t0 = ~0ull, tend = 0;
+    for (int c = 0; c < G; ++c) { t0 = std::min(t0, ph[c][0]); tend = std::max(tend, ph[c][7]); }
+    auto us = [&](int c, int i) { return (ph[c][i] - t0) / 1e3; };
+    double lastStart = 0, avgZero = 0, avgMain = 0, mainMin = 1e9, mainMax = 0, avgFlush = 0;
+    int lastCta = -1;
+    for (int c = 0; c < G; ++c) {
+        lastStart = std::max(lastStart, us(c, 0));
+        avgZero += us(c, 1) - us(c, 0);
+        avgMain += us(c, 2) - us(c, 1);
+        mainMin = std::min(mainMin, us(c, 2)); mainMax = std::max(mainMax, us(c, 2));
+        avgFlush += us(c, 3) - us(c, 2);
+        if (ph[c][4] > ph[c][0] && ph[c][4] >= ph[c][3]) lastCta = c;
+    }
+    printf("last CTA start +%.2f us; avg zero %.2f; avg main %.2f; main done min %.2f max %.2f; avg flush %.2f; total %.2f us\n",
+           lastStart, avgZero / G, avgMain / G, mainMin, mainMax, avgFlush / G, (tend - t0) / 1e3);
+    {
+        static unsigned smid[2048];
+        cudaMemcpyFromSymbol(smid, g_smid, sizeof(smid));
+        std::vector<std::pair<double, int>> v;
+        for (int c = 0; c < G; ++c) v.push_back({us(c, 2) - us(c, 1), c});
+        std::sort(v.begin(), v.end());
+        printf("main-loop us by CTA (sorted): ");
+        for (int i = 0; i < (int)v.size(); i += std::max(1, (int)v.size() / 16)) printf("%.1f ", v[i].first);
+        printf("| max %.1f\nslowest CTAs (cta/sm): ", v.back().first);
+        for (int i = (int)v.size() - 1; i >= std::max(0, (int)v.size() - 8); --i) printf("%d/%u ", v[i].second, smid[v[i].second]);
+        printf("\nfastest CTAs (cta/sm): ");
+        for (int i = 0; i < std::min(8, (int)v.size()); ++i) printf("%d/%u ", v[i].second, smid[v[i].second]);
+        printf("\n");
+    }
+    if (lastCta >= 0)
+        printf("tail CTA %d: flush done %.2f, acc read %.2f, scans+mean %.2f, select %.2f, end %.2f us\n", lastCta,
+               us(lastCta, 3), us(lastCta, 4), us(lastCta, 5), us(lastCta, 6), us(lastCta, 7));
+    return 0;
+}
