@@ -167,25 +167,37 @@ __device__ __forceinline__ void corr_add(unsigned char* corr, uint32_t lane4, ui
     atomicAdd(reinterpret_cast<int*>(corr + (v << 7) + lane4), d);
 }
 
-__device__ __forceinline__ void border_terms(unsigned char* corr, uint32_t lane4, const StepGeom& g,
+struct StripedCorr {  // K1: lane-striped corr (conflict free)
+    unsigned char* base;
+    uint32_t lane4;
+    __device__ __forceinline__ void operator()(uint32_t v, int d) const { corr_add(base, lane4, v, d); }
+};
+
+struct PlainCorr {  // K5: one 256-entry corr array per image group
+    int* base;
+    __device__ __forceinline__ void operator()(uint32_t v, int d) const { atomicAdd(base + v, d); }
+};
+
+template <class CorrAdd>
+__device__ __forceinline__ void border_terms(const CorrAdd& corr, const StepGeom& g,
                                              uint32_t (&c)[4], uint32_t (&n)[4], uint32_t& rn,
                                              bool has_down)
 {
     const int e = g.w - 1 - g.x0;  // index of the last real pixel if < 16
     if (g.x0 == 0)
-        corr_add(corr, lane4, c[0] & 0xFFu, 1);
+        corr(c[0] & 0xFFu, 1);
     // +1 (band-first row: no owned up pair), -1 (last image row: missing down
     // pair +1, fake equal down pair -2); both at once cancel.
     const int dcur = (g.y == 0 ? 1 : 0) - (has_down ? 0 : 1);
     if (dcur != 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-            corr_add(corr, lane4, byte_at(c, i), i <= e ? dcur : 0);
+            corr(byte_at(c, i), i <= e ? dcur : 0);
     }
     if (has_down && g.y + 1 == g.band_rows) {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-            corr_add(corr, lane4, byte_at(n, i), i <= e ? -1 : 0);
+            corr(byte_at(n, i), i <= e ? -1 : 0);
     }
     if (e <= 15) {
         const uint32_t v = byte_dyn(c, e);
@@ -193,7 +205,7 @@ __device__ __forceinline__ void border_terms(unsigned char* corr, uint32_t lane4
         if (has_down)
             fill_tail(n, e, v);
         rn = v;
-        corr_add(corr, lane4, v, -1);
+        corr(v, -1);
     }
     if (!has_down) {
 #pragma unroll
@@ -226,6 +238,102 @@ __device__ __forceinline__ void warp_prefix256(const long long* in, long long* o
 #pragma unroll
     for (int j = 0; j < 8; ++j)
         out[lane * 8 + j] = a[j] + excl;
+}
+
+// Count and sum of one curve from its 512 combinations, by one warp, lane
+// owning thresholds [8*lane, 8*lane+8): card = prefix(cd), sum =
+// prefix(prefix(h2)).  cd(t)/h2(u) are functors; results go to card[]/sum[].
+template <class CD, class H2>
+__device__ __forceinline__ void warp_curve256(CD cd, H2 h2, uint64_t* card, uint64_t* sum)
+{
+    const int lane = threadIdx.x & 31;
+    long long a[8], g[8];
+    long long ra = 0, rg = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        ra += cd(lane * 8 + j);
+        a[j] = ra;
+        rg += h2(lane * 8 + j);
+        g[j] = rg;
+    }
+    long long xa = ra, xg = rg;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long ya = __shfl_up_sync(0xFFFFFFFFu, xa, off);
+        const long long yg = __shfl_up_sync(0xFFFFFFFFu, xg, off);
+        if (lane >= off) {
+            xa += ya;
+            xg += yg;
+        }
+    }
+    const long long ea = xa - ra, eg = xg - rg;
+    long long rs = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        a[j] += ea;
+        g[j] += eg;
+        rs += g[j];
+        g[j] = rs;
+    }
+    long long xs = rs;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long ys = __shfl_up_sync(0xFFFFFFFFu, xs, off);
+        if (lane >= off)
+            xs += ys;
+    }
+    const long long es = xs - rs;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        card[lane * 8 + j] = (uint64_t)a[j];
+        sum[lane * 8 + j] = (uint64_t)(g[j] + es);
+    }
+}
+
+// Same as warp_curve256 but returns each lane's 8 (card, sum) in registers.
+template <class CD, class H2>
+__device__ __forceinline__ void warp_curve256_regs(CD cd, H2 h2, uint64_t (&card)[8],
+                                                   uint64_t (&sum)[8])
+{
+    const int lane = threadIdx.x & 31;
+    long long a[8], g[8];
+    long long ra = 0, rg = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        ra += cd(lane * 8 + j);
+        a[j] = ra;
+        rg += h2(lane * 8 + j);
+        g[j] = rg;
+    }
+    long long xa = ra, xg = rg;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long ya = __shfl_up_sync(0xFFFFFFFFu, xa, off);
+        const long long yg = __shfl_up_sync(0xFFFFFFFFu, xg, off);
+        if (lane >= off) {
+            xa += ya;
+            xg += yg;
+        }
+    }
+    const long long ea = xa - ra, eg = xg - rg;
+    long long rs = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        card[j] = (uint64_t)(a[j] + ea);
+        rs += g[j] + eg;
+        g[j] = rs;
+    }
+    long long xs = rs;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long ys = __shfl_up_sync(0xFFFFFFFFu, xs, off);
+        if (lane >= off)
+            xs += ys;
+    }
+    const long long es = xs - rs;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        sum[j] = (uint64_t)(g[j] + es);
 }
 
 // The 512 linear combinations one partial contributes: cd[v] (count first

@@ -276,11 +276,20 @@ struct Segment {
     uint32_t rn;
 };
 
+// Geometry both accumulation kernels need per segment.
+struct Geo {
+    size_t pitch;
+    int w;
+    int band_rows;  // own rows
+    int r0;         // global row of buffer row 0
+    int h_total;    // global image height
+};
+
 // Loads of one lane's segment at band-relative (y, seg): the row, the row
 // below (when the pair exists) and the right-neighbour byte (when inside the
 // row).  No shuffles: every load is issued a unit ahead of its use.
 template <bool VEC>
-__device__ __forceinline__ void fetch(const WideParams& p, const uint8_t* base, int y, int seg,
+__device__ __forceinline__ void fetch(const Geo& p, const uint8_t* base, int y, int seg,
                                       Segment& s)
 {
     const int x0 = seg << 4;
@@ -304,23 +313,40 @@ __device__ __forceinline__ void zero_hist(unsigned char* sm, int tid)
         zc[i] = make_uint4(0, 0, 0, 0);
 }
 
-// Accumulate one lane's segment.  Warp-uniform fast path when every lane is
-// interior (no border terms); otherwise each border lane fixes itself up.
-__device__ __forceinline__ void process(const WideParams& p, unsigned char* sm, int y, int seg,
-                                        uint32_t lane4, Segment& s)
+// Accumulate one lane's segment.
+// ALIGNED (w % 16 == 0): row starts / row ends are fixed inline with
+// predicated, conflict-free corr updates (a row-end segment has no garbage
+// bytes: its right neighbour becomes its own last pixel, corr -1; a row start
+// has no left pair, corr +1), so only lanes in the band's first row, the
+// image's last row or the halo row take the divergent border_terms path.
+// General widths: every non-interior lane takes border_terms.
+template <bool ALIGNED, class CorrAdd>
+__device__ __forceinline__ void process(const Geo& p, unsigned char* sm, int y, int seg,
+                                        uint32_t lane4, Segment& s, const CorrAdd& corr)
 {
     const int x0 = seg << 4;
     const bool active = y < p.band_rows;
-    const bool interior = active && x0 != 0 && x0 + 16 < p.w && y != 0 && y + 1 < p.band_rows;
-    if (!__all_sync(0xFFFFFFFFu, interior)) {
-        if (active && !interior) {
-            const int gy = p.r0 + y;
-            StepGeom geom{p.w, y, p.band_rows, gy, p.h_total, x0};
-            border_terms(sm + kSmCorr, lane4, geom, s.c, s.n, s.rn,
-                         gy + 1 < p.h_total);
-        }
+    const bool rows_ok = y != 0 && y + 1 < p.band_rows;
+    const bool inner = ALIGNED ? (active && rows_ok)
+                               : (active && rows_ok && x0 != 0 && x0 + 16 < p.w);
+    if (!__all_sync(0xFFFFFFFFu, inner)) {
         if (!active)
             return;
+        if (!inner && (!ALIGNED || !rows_ok)) {
+            const int gy = p.r0 + y;
+            StepGeom geom{p.w, y, p.band_rows, gy, p.h_total, x0};
+            border_terms(corr, geom, s.c, s.n, s.rn, gy + 1 < p.h_total);
+            accumulate_segment(sm, s.c, s.n, s.rn, lane4);
+            return;
+        }
+    }
+    if (ALIGNED) {
+        if (x0 == 0)
+            corr(s.c[0] & 0xFFu, 1);
+        if (x0 + 16 >= p.w) {
+            s.rn = s.c[3] >> 24;
+            corr(s.rn, -1);
+        }
     }
     accumulate_segment(sm, s.c, s.n, s.rn, lane4);
 }
@@ -333,13 +359,15 @@ __device__ __forceinline__ void unit_pos(const WideParams& p, long long u, int l
     seg = (int)(g - q * (unsigned long long)p.nseg);
 }
 
-template <bool VEC>
+template <bool VEC, bool ALIGNED>
 __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const uint32_t lane4 = (uint32_t)lane * 4u;
+    const Geo geo{p.pitch, p.w, p.band_rows, p.r0, p.h_total};
+    const StripedCorr scorr{sm + kSmCorr, lane4};
     phase(0);
 
 #ifdef KOHLER_PHASES
@@ -375,7 +403,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams 
             Segment A, B;
             A.rn = B.rn = 0;
             if (rem > 0)
-                fetch<VEC>(p, base, c0.y, c0.seg, A);
+                fetch<VEC>(geo, base, c0.y, c0.seg, A);
             if (!zeroed) {
                 // overlap the first loads with clearing the histogram
                 zero_hist(sm, tid);
@@ -387,15 +415,15 @@ __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams 
             c1.advance(p.nseg, aq, ar);
             while (rem > 0) {
                 if (rem > 1)
-                    fetch<VEC>(p, base, c1.y, c1.seg, B);
-                process(p, sm, c0.y, c0.seg, lane4, A);
+                    fetch<VEC>(geo, base, c1.y, c1.seg, B);
+                process<ALIGNED>(geo, sm, c0.y, c0.seg, lane4, A, scorr);
                 if (--rem == 0)
                     break;
                 c0 = c1;
                 c0.advance(p.nseg, aq, ar);
                 if (rem > 1)
-                    fetch<VEC>(p, base, c0.y, c0.seg, A);
-                process(p, sm, c1.y, c1.seg, lane4, B);
+                    fetch<VEC>(geo, base, c0.y, c0.seg, A);
+                process<ALIGNED>(geo, sm, c1.y, c1.seg, lane4, B, scorr);
                 --rem;
                 c1 = c0;
                 c1.advance(p.nseg, aq, ar);
@@ -412,6 +440,221 @@ __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams 
     if (!flushed)
         pdl_trigger();
     phase(7);
+}
+
+// ---------------------------------------------------------------------------
+// K5 tile_kernel: batches of small images.  The 32 lane copies of the striped
+// histogram are split into NG = 32/LG groups of LG lanes; group g of every
+// warp accumulates image i0+g, so one CTA accumulates NG whole images at once
+// and pays ONE histogram flush per NG images.  Each image is owned by a
+// single CTA, so its curve is rebuilt in the CTA (no global accumulators, no
+// tickets) and written straight to the outputs; selection runs in a
+// throughput pass (select_kernel, one warp per curve) right after.
+// ---------------------------------------------------------------------------
+struct TileParams {
+    const uint8_t* px;
+    size_t pitch;
+    size_t image_stride;
+    int n;
+    int w;
+    int h;
+    int nseg;
+    int segs;  // h * nseg
+    uint64_t* sums;
+    uint64_t* cards;
+};
+
+constexpr uint32_t kTileCorr = kStripedBytes;  // int[256][32] lane-striped
+// Per image group, the reduced histograms in a padded layout that makes the
+// lane-blocked reads of warp_curve256 bank-conflict free: hist/hhi/corr at
+// pad8(x) = x + (x >> 5) (264 words each), hs at pad16(s) = s + (s >> 4) (544).
+constexpr int kTileGroupWords = 264 * 3 + 544;                       // 1336
+constexpr uint32_t kTileTot = kTileCorr + 32768;                     // u32[NG][1336]
+constexpr uint32_t kTileBytes = kTileTot + 8 * kTileGroupWords * 4;  // ~203 KiB
+
+__device__ __forceinline__ int pad8(int x) { return x + (x >> 5); }
+__device__ __forceinline__ int pad16(int x) { return x + (x >> 4); }
+
+template <bool VEC, bool ALIGNED, int LG>
+__global__ void __launch_bounds__(kWideThreads, 1) tile_kernel(const TileParams p)
+{
+    constexpr int NG = 32 / LG;
+    constexpr int TG = 32 * LG;  // threads per image group
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int g = lane / LG;
+    const int tg = warp * LG + (lane % LG);
+    const uint32_t lane4 = (uint32_t)lane * 4u;
+    uint32_t* tot = reinterpret_cast<uint32_t*>(sm + kTileTot);
+    const Geo geo{p.pitch, p.w, p.h, 0, p.h};
+    const StripedCorr pcorr{sm + kTileCorr, lane4};
+    const int rounds_steps = (p.segs + TG - 1) / TG;  // warp-uniform trip count
+    const int aq = TG / p.nseg, ar = TG % p.nseg;
+
+    {
+        uint4* z = reinterpret_cast<uint4*>(sm);
+        for (int i = tid; i < (int)((kStripedBytes + 32768) / 16); i += kWideThreads)
+            z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    bool waited = false;
+#ifdef KOHLER_PHASES
+    unsigned long long t_acc = 0, t_red = 0, t_mark = clock64();
+#endif
+
+    // first segment of this thread in image `im` (or an inactive position)
+    auto start_pos = [&](long long im, Cursor& c) {
+        c.y = tg / p.nseg;
+        c.seg = tg - c.y * p.nseg;
+        if (im >= p.n)
+            c.y = p.h;  // inactive lane: no loads, no updates
+    };
+    auto image_base = [&](long long im) {
+        return p.px + (size_t)(im < p.n ? im : 0) * p.image_stride;
+    };
+    const long long stride_i0 = (long long)gridDim.x * NG;
+    Segment A, B;
+    A.rn = B.rn = 0;
+    {
+        Cursor cs0;
+        const long long im0 = (long long)blockIdx.x * NG + g;
+        start_pos(im0, cs0);
+        fetch<VEC>(geo, image_base(im0), cs0.y, cs0.seg, A);
+    }
+
+    for (long long i0 = (long long)blockIdx.x * NG; i0 < p.n; i0 += stride_i0) {
+        const long long img = i0 + g;
+        const uint8_t* base = image_base(img);
+        const long long img_next = img + stride_i0;
+        Cursor c0, c1, cn;
+        start_pos(img, c0);
+        start_pos(img_next, cn);
+        c1 = c0;
+        c1.advance(p.nseg, aq, ar);
+        int rem = rounds_steps;
+        bool next_in_b = false;
+        // A holds the round's first segment (prefetched during the previous
+        // round); the last step prefetches the next round's first segment
+        while (rem > 0) {
+            if (rem > 1)
+                fetch<VEC>(geo, base, c1.y, c1.seg, B);
+            else {
+                fetch<VEC>(geo, image_base(img_next), cn.y, cn.seg, B);
+                next_in_b = true;
+            }
+            process<ALIGNED>(geo, sm, c0.y, c0.seg, lane4, A, pcorr);
+            if (--rem == 0)
+                break;
+            c0 = c1;
+            c0.advance(p.nseg, aq, ar);
+            if (rem > 1)
+                fetch<VEC>(geo, base, c0.y, c0.seg, A);
+            else {
+                fetch<VEC>(geo, image_base(img_next), cn.y, cn.seg, A);
+                next_in_b = false;
+            }
+            process<ALIGNED>(geo, sm, c1.y, c1.seg, lane4, B, pcorr);
+            --rem;
+            c1 = c0;
+            c1.advance(p.nseg, aq, ar);
+        }
+        if (next_in_b)
+            A = B;
+        __syncthreads();
+#ifdef KOHLER_PHASES
+        { const unsigned long long t = clock64(); t_acc += t - t_mark; t_mark = t; }
+#endif
+        {
+            // reduce: thread t owns (row t>>1, half t&1); image group gr's
+            // lanes are the NQ consecutive uint4 [gr*NQ, gr*NQ+NQ) of the row,
+            // visited in an order rotated by t so a warp hits distinct banks
+            constexpr int NQ = LG / 4;
+            const int r = tid >> 1, hf = tid & 1;
+            uint4* row = reinterpret_cast<uint4*>(sm + r * 256 + hf * 128);
+            const int dst = hf ? (r < 256 ? pad8(r) : 264 + pad8(r - 256)) : 2 * 264 + pad16(r);
+#pragma unroll
+            for (int kk = 0; kk < NG; ++kk) {
+                const int gr = (kk + tid) & (NG - 1);
+                uint32_t acc = 0;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint4 v = row[gr * NQ + q];
+                    acc += v.x + v.y + v.z + v.w;
+                    row[gr * NQ + q] = make_uint4(0, 0, 0, 0);
+                }
+                tot[gr * kTileGroupWords + dst] = acc;
+            }
+            if (tid < 256) {
+                int4* cr = reinterpret_cast<int4*>(sm + kTileCorr + tid * 128);
+#pragma unroll
+                for (int kk = 0; kk < NG; ++kk) {
+                    const int gr = (kk + tid) & (NG - 1);
+                    int acc = 0;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int4 v = cr[gr * NQ + q];
+                        acc += v.x + v.y + v.z + v.w;
+                        cr[gr * NQ + q] = make_int4(0, 0, 0, 0);
+                    }
+                    reinterpret_cast<int*>(tot)[gr * kTileGroupWords + 264 * 2 + 544 + pad8(tid)] =
+                        acc;
+                }
+            }
+        }
+        __syncthreads();
+#ifdef KOHLER_PHASES
+        { const unsigned long long t = clock64(); t_red += t - t_mark; t_mark = t; }
+#endif
+        if (!waited) {
+            pdl_wait();  // the previous launch may still read our output buffers
+            waited = true;
+        }
+        if (warp < NG && i0 + warp < p.n) {
+            // one warp per image: exact int64 scans -> curve (K3); the next
+            // round's accumulation of the other warps overlaps this
+            const uint32_t* H = tot + warp * kTileGroupWords;  // hist
+            const uint32_t* Q = H + 264;                       // hhi
+            const uint32_t* S = H + 2 * 264;                   // hs
+            const int* Cc = reinterpret_cast<const int*>(H + 2 * 264 + 544);  // corr
+            const long long im = i0 + warp;
+            uint64_t card[8], sum[8];
+            warp_curve256_regs(
+                [&](int x) {
+                    const int px = pad8(x);
+                    return 4ll * H[px] - Cc[px] - 2ll * Q[px];
+                },
+                [&](int u) -> long long {
+                    if (u == 0)
+                        return 0;
+                    const int pm = pad8(u - 1);
+                    long long r2 = 4ll * H[pm] - Cc[pm] - 2ll * S[pad16(2 * u - 2)] -
+                                   (long long)S[pad16(2 * u - 1)];
+                    if (u >= 2)
+                        r2 -= (long long)S[pad16(2 * u - 3)];
+                    return r2;
+                },
+                card, sum);
+            uint64_t* os = p.sums + (size_t)im * 256 + lane * 8;
+            uint64_t* oc = p.cards + (size_t)im * 256 + lane * 8;
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                *reinterpret_cast<ulonglong2*>(os + j) = make_ulonglong2(sum[j], sum[j + 1]);
+                *reinterpret_cast<ulonglong2*>(oc + j) = make_ulonglong2(card[j], card[j + 1]);
+            }
+        }
+    }
+    if (!waited)
+        pdl_wait();
+    pdl_trigger();
+#ifdef KOHLER_PHASES
+    if (tid == 0 && blockIdx.x < 2048) {
+        g_phase[blockIdx.x][0] = t_acc;
+        g_phase[blockIdx.x][1] = t_red;
+        g_phase[blockIdx.x][2] = clock64() - t_mark;
+    }
+#endif
 }
 
 // Definition-level oracle kernel: block t scans every
@@ -484,6 +727,7 @@ struct SelectParams {
 __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
+    pdl_wait();  // curves may come from the preceding (PDL-overlapped) launch
     const int n = p.levels;
     const int cidx = blockIdx.x;
     double* val = reinterpret_cast<double*>(sm);
@@ -582,6 +826,7 @@ struct kohler_cuda_ctx {
     DevBuf tickets;  // zero-initialised, self-cleaning
     DevBuf img;      // staging for host images
     DevBuf out;      // staging for host outputs
+    DevBuf curves;   // K5 curve scratch when the caller wants no curves
     int last_launches = 0;
     bool wide_attr_set = false;
     bool select_attr_set = false;
@@ -687,9 +932,13 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
                      (n == 1 || image_stride % 16 == 0);
     // the smem opt-in is per device; remember it per context
     if (!ctx->wide_attr_set) {
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true>,
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false>,
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         ctx->wide_attr_set = true;
     }
@@ -703,13 +952,35 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (vec)
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true>, p));
+    const bool aligned = w % 16 == 0;
+    if (vec && aligned)
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true, true>, p));
+    else if (vec)
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true, false>, p));
+    else if (aligned)
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false, true>, p));
     else
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false>, p));
+        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false, false>, p));
     KC_CUDA(cudaGetLastError());
     ctx->last_launches += 1;
     return KOHLER_OK;
+}
+
+template <class Kern, class Arg>
+cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                       const Arg& arg)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, arg);
 }
 
 int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t stream)
@@ -722,11 +993,94 @@ int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t str
                                      (int)(kMaxSelectLevels * (8 * 3 + 4 * 2 + 1))));
         ctx->select_attr_set = true;
     }
-    select_kernel<<<sp.n_curves, 32, smem, stream>>>(sp);
-    KC_CUDA(cudaGetLastError());
+    KC_CUDA(launch_pdl(select_kernel, (unsigned)sp.n_curves, 32, smem, stream, sp));
     ctx->last_launches += 1;
     return KOHLER_OK;
 }
+
+template <bool VEC, int LG>
+int launch_tile_t(kohler_cuda_ctx* ctx, const TileParams& tp, unsigned G, cudaStream_t stream)
+{
+    static bool attr_set = false;  // per process; the attribute is per function
+    if (!attr_set) {
+        KC_CUDA(cudaFuncSetAttribute(tile_kernel<VEC, true, LG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+        KC_CUDA(cudaFuncSetAttribute(tile_kernel<VEC, false, LG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+        attr_set = true;
+    }
+    if (tp.w % 16 == 0)
+        KC_CUDA(launch_pdl(tile_kernel<VEC, true, LG>, G, kWideThreads, kTileBytes, stream, tp));
+    else
+        KC_CUDA(launch_pdl(tile_kernel<VEC, false, LG>, G, kWideThreads, kTileBytes, stream, tp));
+    return KOHLER_OK;
+}
+
+// Batches of small images: K5 tile_kernel (curves) + select_kernel (K4).
+int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
+                size_t image_stride, int k, int select, const BatchOut& o, cudaStream_t stream)
+{
+    int ng = 8;
+    while (ng > 1 && ng > n)
+        ng >>= 1;
+    const int lg = 32 / ng;
+    TileParams tp{};
+    tp.px = px;
+    tp.pitch = pitch;
+    tp.image_stride = image_stride;
+    tp.n = n;
+    tp.w = w;
+    tp.h = h;
+    tp.nseg = (w + 15) / 16;
+    tp.segs = h * tp.nseg;
+    tp.sums = o.sums;
+    tp.cards = o.cards;
+    if (!tp.sums) {
+        int rc = ctx->curves.ensure((size_t)n * 512 * sizeof(uint64_t));
+        if (rc)
+            return rc;
+        tp.sums = static_cast<uint64_t*>(ctx->curves.p);
+        tp.cards = tp.sums + (size_t)n * 256;
+    }
+    const long long groups = (n + ng - 1) / ng;
+    const unsigned G = (unsigned)std::max(1ll, std::min<long long>(groups, ctx->sm_count));
+    const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
+                     (image_stride % 16 == 0);
+    int rc = KOHLER_OK;
+    switch (lg * 2 + (vec ? 1 : 0)) {
+    case 4 * 2 + 1: rc = launch_tile_t<true, 4>(ctx, tp, G, stream); break;
+    case 4 * 2: rc = launch_tile_t<false, 4>(ctx, tp, G, stream); break;
+    case 8 * 2 + 1: rc = launch_tile_t<true, 8>(ctx, tp, G, stream); break;
+    case 8 * 2: rc = launch_tile_t<false, 8>(ctx, tp, G, stream); break;
+    case 16 * 2 + 1: rc = launch_tile_t<true, 16>(ctx, tp, G, stream); break;
+    case 16 * 2: rc = launch_tile_t<false, 16>(ctx, tp, G, stream); break;
+    case 32 * 2 + 1: rc = launch_tile_t<true, 32>(ctx, tp, G, stream); break;
+    default: rc = launch_tile_t<false, 32>(ctx, tp, G, stream); break;
+    }
+    if (rc)
+        return rc;
+    ctx->last_launches += 1;
+    if (select || o.values || o.defined) {
+        SelectParams sp{};
+        sp.sums = tp.sums;
+        sp.cards = tp.cards;
+        sp.n_curves = n;
+        sp.levels = 256;
+        sp.k = k;
+        sp.want_select = select;
+        sp.values = o.values;
+        sp.defined = o.defined;
+        sp.t0s = o.t0s;
+        sp.topks = o.topks;
+        sp.topk_counts = o.topk_counts;
+        sp.status = o.status;
+        rc = launch_select(ctx, sp, stream);
+    }
+    return rc;
+}
+
+// Small images in batches go to K5, everything else to K1.
+bool use_tile(int n, int w, int h) { return n >= 2 && (long long)w * h <= 65536; }
 
 // Stage a host batch into the device, run, copy results back.
 int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
@@ -770,7 +1124,8 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     d.status = d.topk_counts + n;
     d.topks = d.status + n;
     ctx->last_launches = 0;
-    rc = launch_wide(ctx, dimg, n, w, h, h, 0, dpitch, dstride, k, select, d, st);
+    rc = use_tile(n, w, h) ? launch_tile(ctx, dimg, n, w, h, dpitch, dstride, k, select, d, st)
+                           : launch_wide(ctx, dimg, n, w, h, h, 0, dpitch, dstride, k, select, d, st);
     if (rc)
         return rc;
     if (host.sums)
@@ -847,6 +1202,7 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         ctx->tickets.release();
         ctx->img.release();
         ctx->out.release();
+        ctx->curves.release();
         cudaStreamDestroy(ctx->stream);
     }
     delete ctx;
@@ -953,6 +1309,9 @@ int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, in
     ctx->last_launches = 0;
     BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
     const bool select = t0s || topks || topk_counts || status;
+    if (use_tile(n, w, h))
+        return launch_tile(ctx, px, n, w, h, pitch, image_stride, k, select ? 1 : 0, o,
+                           static_cast<cudaStream_t>(stream));
     return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select ? 1 : 0, o,
                        static_cast<cudaStream_t>(stream));
 }

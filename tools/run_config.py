@@ -1,5 +1,7 @@
-"""Run one config through the device API a few times (for ncu / sanitizer)."""
+"""Run / time one config through the device API (for ncu, sanitizer and the
+per-config throughput table in DESIGN.md)."""
 import argparse
+import json
 import os
 import sys
 
@@ -13,9 +15,17 @@ from paper_1707_05062_b200 import Context, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--time", action="store_true")
 a = ap.parse_args()
 x = synth.generate(a.config, device="cuda")
 n, h, w = x.shape
+copies = 1
+l2 = torch.cuda.get_device_properties(0).L2_cache_size
+if x.numel() < 2 * l2:  # rotate copies so every step reads HBM
+    copies = int(2 * l2 // x.numel()) + 1
+    x = torch.stack([x] * copies)
+else:
+    x = x[None]
 ctx = Context(0)
 k = 6
 out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
@@ -24,7 +34,22 @@ out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
        "topk": torch.zeros((n, k), dtype=torch.int32, device="cuda"),
        "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda"),
        "status": torch.zeros(n, dtype=torch.int32, device="cuda")}
-for _ in range(a.reps):
-    ctx.analyze_batch_device(x, w, h, w, w * h, n, k, out)
+for i in range(a.reps):
+    ctx.analyze_batch_device(x[i % copies], w, h, w, w * h, n, k, out)
 torch.cuda.synchronize()
-print(a.config, "t0[0] =", int(out["t0"][0]), "topk[0] =", out["topk"][0].tolist())
+if a.time:
+    steps = max(3, int(2e9 // max(x[0].numel(), 1)))
+    steps = min(steps, 2000)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        ctx.analyze_batch_device(x[i % copies], w, h, w, w * h, n, k, out)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    px = n * h * w
+    print(json.dumps({"config": a.config, "n": n, "w": w, "h": h, "ms_per_step": ms,
+                      "gpix_per_s": px / ms / 1e6, "hbm_frac": px / ms / 1e6 / 6452.8,
+                      "images_per_s": n / ms * 1e3, "copies": copies, "steps": steps}))
+else:
+    print(a.config, "t0[0] =", int(out["t0"][0]), "topk[0] =", out["topk"][0].tolist())

@@ -1,0 +1,31 @@
+// Debug probe of the K5 tile kernel: per-CTA clock64 totals of the
+// accumulation phase, the reduce phase, and the rest, for n images of w x h.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DKOHLER_PHASES -Iinclude -o tools/tile_probe tools/tile_probe.cu
+#include "../paper_1707_05062_b200/csrc/kohler_kernels.cu"
+#include <vector>
+int main(int argc, char** argv)
+{
+    const int n = argc > 1 ? atoi(argv[1]) : 65536, w = argc > 2 ? atoi(argv[2]) : 128,
+              h = argc > 3 ? atoi(argv[3]) : 128;
+    kohler_cuda_ctx* ctx = nullptr;
+    if (kohler_cuda_create(0, &ctx)) { printf("%s\n", kohler_cuda_last_error()); return 1; }
+    std::vector<uint8_t> img((size_t)n * w * h);
+    uint32_t x = 1;
+    for (auto& v : img) { x = x * 1664525u + 1013904223u; v = (uint8_t)(x >> 24); }
+    uint8_t* d; cudaMalloc(&d, img.size()); cudaMemcpy(d, img.data(), img.size(), cudaMemcpyHostToDevice);
+    uint64_t* sums; cudaMalloc(&sums, (size_t)n * 4096);
+    int* ints; cudaMalloc(&ints, (size_t)n * 64);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(a);
+        kohler_cuda_analyze_batch_device(ctx, d, n, w, h, w, (size_t)w * h, 6, sums, sums + (size_t)n * 256, nullptr, nullptr, ints, ints + n, ints + 2 * n, ints + 3 * n, 0);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b); printf("batch %.3f ms (%.1f Gpx/s)\n", ms, (double)n * w * h / ms / 1e6);
+    }
+    static unsigned long long ph[2048][8];
+    cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
+    double acc = 0, red = 0, rest = 0; int G = 148;
+    for (int c = 0; c < G; ++c) { acc += ph[c][0]; red += ph[c][1]; rest += ph[c][2]; }
+    printf("per CTA cycles: accumulate %.0f, reduce %.0f, other %.0f\n", acc / G, red / G, rest / G);
+    return 0;
+}
