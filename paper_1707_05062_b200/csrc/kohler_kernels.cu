@@ -26,6 +26,7 @@
 
 #include "kohler_cuda.h"
 #include "kohler_device.cuh"
+#include "kohler_walk.cuh"
 
 using namespace kohler_dev;
 
@@ -42,17 +43,20 @@ struct WideParams {
     int n;          // images
     int w;          // width
     int band_rows;  // own rows per image (band)
+    int buf_rows;   // rows present in the buffer (own rows + halo row if any)
     int h_total;    // global height
     int r0;         // global row of buffer row 0
-    int nseg;       // 16-pixel segments per row
-    long long upi;  // units (32 segments) per image
-    long long total_units;
+    int nseg;       // S: 16-pixel segments per row
+    int R;          // rows per column walk (even)
+    long long T;    // walk tasks per image (S * ceil(band_rows / R))
+    long long gpi;  // 32-lane groups per image
+    long long total_groups;
+    int epoch;      // max groups between W spills (kohler_walk::kMaxEventsPerWord)
+    unsigned long long seg_magic;  // floor(2^64 / nseg) + 1 (nseg > 1)
+    long long cta_q, cta_r;        // total_groups = cta_q * G + cta_r
     unsigned long long* acc;  // [n][copies][512]
     int copies;
     unsigned* tickets;  // [n]
-    unsigned long long seg_magic;  // floor(2^64 / nseg) + 1 (nseg > 1)
-    int adv_q, adv_r;              // 32 = adv_q * nseg + adv_r (one unit)
-    long long cta_q, cta_r;        // U = cta_q * G + cta_r (CTA range sizes)
     int k;
     int select;
     uint64_t* sums;
@@ -65,16 +69,33 @@ struct WideParams {
     int* status;
 };
 
-// Shared-memory map of K1 (dynamic).
-constexpr uint32_t kSmCorr = kStripedBytes;                 // int[256][32] lane-striped
-constexpr uint32_t kSmCorrCopy = kSmCorr + 32768;           // int[256]
-constexpr uint32_t kSmTot = kSmCorrCopy + 1024;             // u64[1024]
-constexpr uint32_t kSmVal = kSmTot + 8192;                  // i64[512]
-constexpr uint32_t kSmCurve = kSmVal + 4096;                // u64 sum[256], card[256]
-constexpr uint32_t kSmMean = kSmCurve + 4096;               // f64[256]
-constexpr uint32_t kSmDef = kSmMean + 2048;                 // u8[256]
-constexpr uint32_t kSmScratch = kSmDef + 256;               // rv,rt,mv,mt [256]
-constexpr uint32_t kSmWideBytes = kSmScratch + 256 * (8 + 4 + 8 + 4);
+#ifndef KOHLER_WALK_THREADS
+#define KOHLER_WALK_THREADS 384
+#endif
+constexpr int kWalkThreads = KOHLER_WALK_THREADS;
+constexpr int kWalkWarps = kWalkThreads / 32;
+
+// Shared-memory map of K1 (dynamic), after the striped counters and corr
+// (kohler_walk.cuh).
+constexpr uint32_t kSmWacc = kohler_walk::kCorr + kohler_walk::kCorrBytes;  // u64 [2 copies][2 fields][256]
+constexpr uint32_t kSmHsTot = kSmWacc + 8192;        // u64[512]
+constexpr uint32_t kSmCorrTot = kSmHsTot + 4096;     // int[256]
+// Row ring of the column walks (cp.async destination): per warp kRingSlots
+// slots of 32 lane segments + a 16-byte pad on each side.  Idle during the
+// flush, so the reconstruction / selection scratch aliases it.
+constexpr int kRingSlots = 4;
+constexpr uint32_t kSlotBytes = 16 + 32 * 16 + 16;
+constexpr uint32_t kSmRing = kSmCorrTot + 1024;
+constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlotBytes;
+constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
+constexpr uint32_t kSmCurve = kSmVal + 4096;         // u64 sum[256], card[256]
+constexpr uint32_t kSmMean = kSmCurve + 4096;        // f64[256]
+constexpr uint32_t kSmDef = kSmMean + 2048;          // u8[256]
+constexpr uint32_t kSmScratch = kSmDef + 256;        // block_select256 scratch
+constexpr uint32_t kSmFinishEnd = kSmScratch + 256 * (8 + 4 + 8 + 4);
+constexpr uint32_t kSmWideBytes =
+    kSmRing + kRingBytes > kSmFinishEnd ? kSmRing + kRingBytes : kSmFinishEnd;
+static_assert(kSmWideBytes <= 227 * 1024, "K1 shared memory");
 
 // CTA owning unit u under the balanced partition (first cta_r CTAs hold
 // cta_q + 1 units, the rest cta_q).
@@ -95,6 +116,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ unsigned long long g_phase[2048][8];
 __device__ unsigned g_smid[2048];
 __device__ int g_rot;
+__device__ unsigned long long g_wend[2048][32];  // per-warp end of its last walk
 __device__ __forceinline__ void phase(int i)
 {
     if (threadIdx.x == 0 && blockIdx.x < 2048) {
@@ -108,12 +130,21 @@ __device__ __forceinline__ void phase(int i)
         }
     }
 }
+__device__ __forceinline__ void warp_end()
+{
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 2048) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_wend[blockIdx.x][threadIdx.x >> 5] = t;
+    }
+}
 #else
 __device__ __forceinline__ void phase(int) {}
+__device__ __forceinline__ void warp_end() {}
 #endif
 
 // Last CTA of an image: sum accumulator copies, reset them, rebuild the
-// curve, write it, and (optionally) select.
+// curve (K3: int64 prefix scans), write it, and (optionally) select (K4).
 __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
 {
     const int tid = threadIdx.x;
@@ -123,8 +154,8 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
     double* mean = reinterpret_cast<double*>(sm + kSmMean);
     uint8_t* def = sm + kSmDef;
 
-    if (tid < 512) {
-        unsigned long long* a = p.acc + (size_t)img * p.copies * 512 + tid;
+    for (int r = tid; r < 512; r += kWalkThreads) {
+        unsigned long long* a = p.acc + (size_t)img * p.copies * 512 + r;
         unsigned long long v[kAccCopiesSingle];
 #pragma unroll
         for (int c = 0; c < kAccCopiesSingle; ++c)
@@ -136,14 +167,14 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
             if (c < p.copies)
                 __stcg(a + c * 512, 0ull);
         }
-        sval[tid] = (long long)s;
+        sval[r] = (long long)s;
     }
     if (tid == 0)
         p.tickets[img] = 0;
     __syncthreads();
     phase(4);
     const int warp = tid >> 5;
-    long long* tmp = reinterpret_cast<long long*>(sm + kSmTot);  // reuse
+    long long* tmp = reinterpret_cast<long long*>(sm + kSmHsTot);  // free here
     if (warp == 0)
         warp_prefix256(sval, reinterpret_cast<long long*>(ccard));
     else if (warp == 1) {
@@ -179,66 +210,94 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
     phase(6);
 }
 
-// CTA flush of one image's partial: reduce the striped histogram (zeroing it
-// for the next image), form the 512 combinations, REDG them, take a ticket.
+// Fold the packed W words (both copies) into the u64 per-CTA accumulators
+// and clear them.  Thread t owns (copy t >> 8, key t & 255): 32 lane words
+// read rotated by t & 7 so a warp's LDS.128 hit distinct bank quads.
+__device__ __forceinline__ void spill_w(unsigned char* sm, int tid)
+{
+    using namespace kohler_walk;
+    const int copy = tid >> 8, key = tid & 255;
+    uint4* row = reinterpret_cast<uint4*>(sm + (key + 256 * copy) * 256 + 128);
+    uint32_t h = 0, b = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint4 v = row[(j + tid) & 7];
+        h += (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
+        b += (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
+        row[(j + tid) & 7] = make_uint4(0, 0, 0, 0);
+    }
+    unsigned long long* wacc = reinterpret_cast<unsigned long long*>(sm + kSmWacc);
+    wacc[copy * 512 + key] += h;        // hist field
+    wacc[copy * 512 + 256 + key] += b;  // B field
+}
+
+// CTA flush of one image's partial: reduce the striped counters (clearing
+// them for the next image), form the 512 combinations, REDG them, take a
+// ticket; the last CTA of the image finishes it.
 __device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
 {
+    using namespace kohler_walk;
     const int tid = threadIdx.x;
-    int* corr_copy = reinterpret_cast<int*>(sm + kSmCorrCopy);
-    unsigned long long* tot = reinterpret_cast<unsigned long long*>(sm + kSmTot);
-
-    {
-        // thread t owns (row t>>1, half t&1): 32 lane words, read rotated
-        // by t&7 so a warp's LDS.128 hit distinct bank quads.
-        uint4* row = reinterpret_cast<uint4*>(sm + (tid >> 1) * 256 + (tid & 1) * 128);
-        uint4 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            v[j] = row[(j + tid) & 7];
+    unsigned long long* hs_tot = reinterpret_cast<unsigned long long*>(sm + kSmHsTot);
+    int* corr_tot = reinterpret_cast<int*>(sm + kSmCorrTot);
+    unsigned long long* wacc = reinterpret_cast<unsigned long long*>(sm + kSmWacc);
+    for (int t = tid; t < 512; t += kWalkThreads) {
+        uint4* row = reinterpret_cast<uint4*>(sm + t * 256);  // half 0: Hs[t] / dummy
         unsigned long long s = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            s += (unsigned long long)v[j].x + v[j].y + v[j].z + v[j].w;
-            row[(j + tid) & 7] = make_uint4(0, 0, 0, 0);
+            const uint4 v = row[(j + t) & 7];
+            s += (unsigned long long)v.x + v.y + v.z + v.w;
+            row[(j + t) & 7] = make_uint4(0, 0, 0, 0);
         }
-        tot[tid] = s;
-        if (tid < 256) {
-            // corr row tid: 32 lane words, same rotation
-            int4* cr = reinterpret_cast<int4*>(sm + kSmCorr + tid * 128);
-            int4 q[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                q[j] = cr[(j + tid) & 7];
+        hs_tot[t] = s;
+        spill_w(sm, t);
+        if (t < 256) {
+            int4* cr = reinterpret_cast<int4*>(sm + kCorr + t * 128);
             int cs = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                cs += q[j].x + q[j].y + q[j].z + q[j].w;
-                cr[(j + tid) & 7] = make_int4(0, 0, 0, 0);
+                const int4 q = cr[(j + t) & 7];
+                cs += q.x + q.y + q.z + q.w;
+                cr[(j + t) & 7] = make_int4(0, 0, 0, 0);
             }
-            corr_copy[tid] = cs;
+            corr_tot[t] = cs;
         }
     }
     __syncthreads();
-    // the workspace (acc, tickets, chunk counters) and outputs may still be in
-    // use by the previous launch in this stream
+    // the workspace (acc, tickets) and outputs may still be in use by the
+    // previous launch in this stream
     pdl_wait();
-    if (tid < 512) {
-        const long long v = combo(
-            tid, [&](int x) { return tot[2 * x + 1]; },
-            [&](int x) { return tot[2 * (256 + x) + 1]; }, [&](int x) { return tot[2 * x]; },
-            [&](int x) { return corr_copy[x]; });
-        if (v != 0) {
+    for (int t = tid; t < 512; t += kWalkThreads) {
+        auto hist = [&](int v) { return (long long)(wacc[v] + wacc[512 + v]); };
+        long long val;
+        if (t < 256) {
+            const long long bs = (long long)(wacc[256 + t] + wacc[512 + 256 + t]);
+            val = bs - 4ll * hist(t);  // card first difference
+        } else {
+            const int u = t - 256;  // sum second difference
+            if (u == 0) {
+                val = 0;
+            } else {
+                val = 4ll * hist(u - 1) - (long long)corr_tot[u - 1] -
+                      2ll * (long long)hs_tot[2 * u - 2] - (long long)hs_tot[2 * u - 1];
+                if (u >= 2)
+                    val -= (long long)hs_tot[2 * u - 3];
+            }
+        }
+        if (val != 0) {
             const int copy = blockIdx.x % p.copies;
-            atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + tid,
-                      (unsigned long long)v);
+            atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + t, (unsigned long long)val);
         }
     }
     __threadfence();
     __syncthreads();
+    for (int t = tid; t < 1024; t += kWalkThreads)
+        wacc[t] = 0;
     __shared__ int s_last;
     if (tid == 0) {
-        const long long first = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
-        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, p.cta_q, p.cta_r);
+        const long long first = cta_of_unit((long long)img * p.gpi, p.cta_q, p.cta_r);
+        const long long last = cta_of_unit((long long)(img + 1) * p.gpi - 1, p.cta_q, p.cta_r);
         const unsigned expected = (unsigned)(last - first + 1);
         const unsigned prev = atomicAdd(p.tickets + img, 1u);
         s_last = (prev + 1 == expected);
@@ -303,16 +362,6 @@ __device__ __forceinline__ void fetch(const Geo& p, const uint8_t* base, int y, 
     }
 }
 
-__device__ __forceinline__ void zero_hist(unsigned char* sm, int tid)
-{
-    uint4* z = reinterpret_cast<uint4*>(sm);
-    for (int i = tid; i < (int)(kStripedBytes / 16); i += kWideThreads)
-        z[i] = make_uint4(0, 0, 0, 0);
-    uint4* zc = reinterpret_cast<uint4*>(sm + kSmCorr);
-    for (int i = tid; i < 32768 / 16; i += kWideThreads)
-        zc[i] = make_uint4(0, 0, 0, 0);
-}
-
 // Accumulate one lane's segment.
 // ALIGNED (w % 16 == 0): row starts / row ends are fixed inline with
 // predicated, conflict-free corr updates (a row-end segment has no garbage
@@ -351,31 +400,332 @@ __device__ __forceinline__ void process(const Geo& p, unsigned char* sm, int y, 
     accumulate_segment(sm, s.c, s.n, s.rn, lane4);
 }
 
-__device__ __forceinline__ void unit_pos(const WideParams& p, long long u, int lane, int& y, int& seg)
+// ---------------------------------------------------------------------------
+// K1 walk_kernel: persistent, one 512-thread CTA per SM.  Work unit: a
+// "group" of 32 column walks (lane L: task 32g + L of its image, task
+// tau -> segment column tau % S, row chunk tau / S, rows [cR, cR + R)).
+// CTAs own balanced contiguous group ranges; within an image range, epochs of
+// at most p.epoch groups bound the packed W words (kohler_walk.cuh), and each
+// warp walks a balanced contiguous sub-range of the epoch, streaming rows
+// through a 4-slot register ring (3 rows in flight) across group boundaries.
+// ---------------------------------------------------------------------------
+struct LaneGeo {
+    const uint8_t* p;  // row y0 - 1, column x0 (dereferenced only for valid rows)
+    const uint8_t* pl; // p - 1 if the segment has a left neighbour, else p
+    const uint8_t* pr; // p + 16 if the segment has a right neighbour, else p + 15
+    int x0;
+    int y0;            // first own row (band-relative)
+    int nrows;         // own rows of the walk (0: no task)
+    int e;             // index of the last real pixel of the segment if < 16
+    int jlo, jcl;      // ring position j loads row y0 - 1 + clamp(j, jlo, jcl)
+};
+
+__device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* base, long long g,
+                                            int lane)
 {
-    const unsigned long long g = (unsigned long long)u * 32ull + (unsigned)lane;
-    const unsigned long long q = p.nseg == 1 ? g : __umul64hi(g, p.seg_magic);
-    y = (int)q;
-    seg = (int)(g - q * (unsigned long long)p.nseg);
+    LaneGeo L;
+    const unsigned long long tau = (unsigned long long)g * 32ull + (unsigned)lane;
+    const bool act = tau < (unsigned long long)p.T;
+    const unsigned long long c = p.nseg == 1 ? tau : __umul64hi(tau, p.seg_magic);
+    const int s = (int)(tau - c * (unsigned long long)p.nseg);
+    L.x0 = s << 4;
+    L.e = p.w - 1 - L.x0;
+    if (act) {
+        L.y0 = (int)c * p.R;
+        L.nrows = min(L.y0 + p.R, p.band_rows) - L.y0;
+        L.jlo = L.y0 == 0 ? 1 : 0;
+        // loads past the buffer's last row re-read it: the down row of the
+        // image's last row is the row itself (equal "fake" down pairs)
+        L.jcl = p.buf_rows - L.y0;
+    } else {
+        L.y0 = 1;  // a valid address (row 0), never used
+        L.nrows = 0;
+        L.jlo = 0;
+        L.jcl = 0;
+    }
+    L.p = base + ((long long)L.y0 - 1) * (long long)p.pitch + L.x0;
+    L.pl = L.p - (L.x0 > 0 ? 1 : 0);
+    L.pr = L.p + (L.e > 15 ? 16 : 15);
+    return L;
 }
 
-template <bool VEC, bool ALIGNED>
-__global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams p)
+// Issue the copies of ring position j of a lane's walk into ring slot `dst`
+// (shared address of this lane's 16-byte segment in the slot): the segment,
+// from a clamped valid row, and for lane 0 / lane 31 the 16 bytes left /
+// right of it where that neighbour exists.  One cp.async group per position.
+__device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitch, uint32_t dst,
+                                         int lane)
+{
+    const uint32_t off = (uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
+    // lane 0 / 31 also copy the 16 bytes left / right of the segment (if the
+    // neighbour exists): predicated, no branch
+    const int d = lane == 0 ? -16 : 16;
+    const uint32_t pad = ((lane == 0 && L.x0 > 0) || (lane == 31 && L.e > 15)) ? 1u : 0u;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+        "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
+        "@p cp.async.cg.shared.global [%3], [%4], 16;\n\t"
+        "cp.async.commit_group;\n\t}" ::"r"(dst),
+        "l"(L.p + off), "r"(pad), "r"(dst + d), "l"(L.p + off + d)
+        : "memory");
+}
+
+// Read ring slot position of this lane back: the segment and its neighbour
+// bytes (a row start's left / a row end's right neighbour is the pixel
+// itself: equal => neutral; lanes next to each other in a warp are
+// horizontal neighbours unless a row boundary lies between them).
+__device__ __forceinline__ void read_row(kohler_walk::Row& r, uint32_t seg, uint32_t offl,
+                                         uint32_t offr)
+{
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "r"(seg)
+                 : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r.ln) : "r"(seg + offl) : "memory");
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r.rn) : "r"(seg + offr) : "memory");
+}
+
+// Per-group, warp-uniform flags.
+struct GroupFlags {
+    bool edge;       // some lane is at a row start or row end (corr terms)
+    bool ragged;     // some lane's segment runs past the row end (garbage bytes)
+    unsigned extra;  // bit j: some lane's row at position j needs border terms
+};
+
+__device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const LaneGeo& L, bool aligned)
+{
+    GroupFlags f;
+    const bool act = L.nrows > 0;
+    f.edge = __any_sync(0xFFFFFFFFu, act && (L.x0 == 0 || L.e <= 15));
+    f.ragged = !aligned && __any_sync(0xFFFFFFFFu, act && L.e < 15);
+    unsigned m = 0;
+    if (act) {
+        // position j processes band row y0 + j - 2
+        if (L.y0 == 0)
+            m |= 1u << 2;  // band first row: up pair missing / not owned
+        if (L.y0 + L.nrows == p.band_rows)
+            m |= 1u << (L.nrows + 1);  // band last row: last image row or halo
+    }
+    f.extra = __reduce_or_sync(0xFFFFFFFFu, m);
+    return f;
+}
+
+// Border rows of a group (rare: the band's first row, the band's last row),
+// done once per group after its walk from a re-read of the rows involved:
+//   band first row      : corr +1 per pixel (up pair missing or not owned)
+//   last image row      : corr -1 per pixel (its down pairs were emitted as
+//                         equal fakes: the down row was the row itself)
+//   halo row (band end) : per halo pixel d under c, its owned up pair as a W
+//                         event B = 4 + sign(c - d) = 5 - q(c -> d), corr +3
+template <bool ALIGNED>
+__device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm, uint32_t smbase,
+                                         const LaneGeo& G, uint32_t lane4)
+{
+    using namespace kohler_walk;
+    if (G.nrows <= 0)
+        return;
+    const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
+    auto load16 = [&](int y, uint32_t (&w)[4]) {
+        const uint8_t* rp = G.p + (size_t)(y - G.y0 + 1) * p.pitch;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                word |= (4 * jj + b < nreal ? (uint32_t)rp[4 * jj + b] : 0u) << (8 * b);
+            w[jj] = word;
+        }
+    };
+    auto byte = [](const uint32_t (&w)[4], int i) { return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu; };
+    if (G.y0 == 0) {
+        uint32_t w[4];
+        load16(0, w);
+        for (int i = 0; i < nreal; ++i)
+            red_add(smbase + kCorr + (byte(w, i) << 7) + lane4, 1u);
+    }
+    const int ylast = G.y0 + G.nrows - 1;
+    if (ylast == p.band_rows - 1) {
+        uint32_t c[4];
+        load16(ylast, c);
+        if (p.r0 + ylast == p.h_total - 1) {
+            for (int i = 0; i < nreal; ++i)
+                red_add(smbase + kCorr + (byte(c, i) << 7) + lane4, 0xFFFFFFFFu);
+        } else {
+            uint32_t d[4];
+            load16(ylast + 1, d);
+            for (int i = 0; i < nreal; ++i) {
+                const uint32_t cv = byte(c, i), dv = byte(d, i);
+                const uint32_t b = 4u + (cv > dv) - (cv < dv);  // 4 + sign(c - d)
+                atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW0 + (dv << 8) + lane4), (b << 16) | 1u);
+                red_add(smbase + kCorr + (dv << 7) + lane4, 3u);
+            }
+        }
+    }
+}
+
+template <bool ALIGNED>
+__device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
+                                           uint32_t smbase, const uint8_t* base, long long ga,
+                                           long long gb, bool zero_first)
+{
+    using namespace kohler_walk;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane4 = (uint32_t)lane * 4u;
+    const uint32_t kneg = smbase - lane4;
+    const uint32_t dummy = smbase + kDummy + lane4;
+    const int P = p.R + 2;  // ring positions per group (rows y0-1 .. y0+R), P % 4 == 0
+    const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
+    const bool any = ga < gb;
+    // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
+    const uint32_t seg0 = smbase + kSmRing + (uint32_t)warp * (kRingSlots * kSlotBytes) + 16u +
+                          (uint32_t)lane * 16u;
+
+    LaneGeo G{};
+    if (any) {
+        G = lane_geo(p, base, ga, lane);
+        fetch_row(G, 0, pitch, seg0, lane);
+        fetch_row(G, 1, pitch, seg0 + kSlotBytes, lane);
+        fetch_row(G, 2, pitch, seg0 + 2 * kSlotBytes, lane);
+    }
+    if (zero_first) {
+        // clear the counters while the first rows are in flight
+        uint4* z = reinterpret_cast<uint4*>(sm);
+        for (int i = threadIdx.x; i < (int)((kHistBytes + kCorrBytes + 8192) / 16); i += kWalkThreads)
+            z[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        phase(1);
+    }
+    if (!any)
+        return;
+
+    Car X, Y;
+    for (long long g = ga; g < gb; ++g) {
+        const bool has_next = g + 1 < gb;
+        LaneGeo N = G;  // next group's geometry, computed before the last block
+        const GroupFlags F = group_flags(p, G, ALIGNED);
+        const bool row_start = G.x0 == 0, row_end = G.e <= 15;
+        const uint32_t offl = G.x0 > 0 ? 0xFFFFFFFFu : 0u;  // left neighbour byte
+        const uint32_t offr = G.e > 15 ? 16u : 15u;         // right neighbour byte
+
+        // One ring position j (slot s = j & 3): prefetch position j + 3 (of
+        // this group or, past its end, of the next), absorb row j into D and
+        // process row j - 1 (C) against it.  WC: W copy of C's row parity.
+        auto step = [&](Car& D, Car& C, int j, auto slot, auto kind, auto wc) {
+            constexpr int S = decltype(slot)::value;
+            constexpr int KIND = decltype(kind)::value;  // 0 absorb, 1 prime, 2 process, 3 process + cross
+            constexpr int WC = decltype(wc)::value;
+            constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
+            constexpr uint32_t kPref = ((S + 3) & 3) * kSlotBytes;
+            // slot S was committed 3 groups ago; <= 2 younger groups may pend
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncwarp();
+            Row r;
+            read_row(r, seg0 + S * kSlotBytes, offl, offr);
+            __syncwarp();  // every lane has read slot S before anyone refills it
+            if (KIND == 3 && j + 3 >= P) {
+                if (has_next)
+                    fetch_row(N, j + 3 - P, pitch, seg0 + kPref, lane);
+                else
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+            } else {
+                fetch_row(G, j + 3, pitch, seg0 + kPref, lane);
+            }
+            absorb<ALIGNED>(D, r, lane4, G.e);
+            if (KIND == 1) {
+                // prime: q(up -> row y0) from row y0 - 1 (neutral at the band's first row)
+                const bool has_up = G.y0 > 0;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    D.ue[jj] = has_up ? qstep(qfrom(C.e[jj]), D.e[jj]) : kNeutral;
+                    D.uo[jj] = has_up ? qstep(qfrom(C.o[jj]), D.o[jj]) : kNeutral;
+                }
+            }
+            if (KIND < 2)
+                return;
+            const bool live = j - 2 < G.nrows;
+            uint32_t qre[4], qro[4], qde[4], qdo[4], Be[4], Bo[4];
+            pair_q(C, D.e, D.o, qre, qro, qde, qdo);
+            b_terms(C, qre, qro, qde, qdo, Be, Bo);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                D.ue[jj] = qde[jj];
+                D.uo[jj] = qdo[jj];
+            }
+            const uint32_t Arn = __byte_perm(C.rn, lane4, 0x5504);
+            if (ALIGNED || !F.ragged) {
+                if (live) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW + C.A[i]), b_of(Be, Bo, i));
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + D.A[i] + kneg);
+                }
+            } else if (live) {
+                // ragged row ends: bytes past the row end neutralised
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const bool real = i <= G.e;
+                    atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW + C.A[i]),
+                              real ? b_of(Be, Bo, i) : 0u);
+                    red_inc(real ? C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg : dummy);
+                    red_inc(real ? C.A[i] + D.A[i] + kneg : dummy);
+                }
+            }
+            if (F.edge && live) {
+                if (row_start)
+                    red_add(corr_addr(smbase, C.A[0], lane4), 1u);
+                if (row_end)
+                    red_add(corr_addr(smbase, Arn, lane4), 0xFFFFFFFFu);
+            }
+        };
+        using K0 = std::integral_constant<int, 0>;
+        using K1 = std::integral_constant<int, 1>;
+        using K2 = std::integral_constant<int, 2>;
+        using K3 = std::integral_constant<int, 3>;
+        using S0 = std::integral_constant<int, 0>;
+        using S1 = std::integral_constant<int, 1>;
+        using S2 = std::integral_constant<int, 2>;
+        using S3 = std::integral_constant<int, 3>;
+        // positions 0..3: absorb row y0-1, prime row y0, process rows y0, y0+1
+        // (W copy = parity of the processed row = parity of j, y0 even)
+        step(X, Y, 0, S0{}, K0{}, S0{});
+        step(Y, X, 1, S1{}, K1{}, S1{});
+        step(X, Y, 2, S2{}, K2{}, S0{});
+        step(Y, X, 3, S3{}, K2{}, S1{});
+        int j = 4;
+        for (; j < P - 4; j += 4) {
+            step(X, Y, j, S0{}, K2{}, S0{});
+            step(Y, X, j + 1, S1{}, K2{}, S1{});
+            step(X, Y, j + 2, S2{}, K2{}, S0{});
+            step(Y, X, j + 3, S3{}, K2{}, S1{});
+        }
+        if (has_next)
+            N = lane_geo(p, base, g + 1, lane);
+        step(X, Y, j, S0{}, K3{}, S0{});
+        step(Y, X, j + 1, S1{}, K3{}, S1{});
+        step(X, Y, j + 2, S2{}, K3{}, S0{});
+        step(Y, X, j + 3, S3{}, K3{}, S1{});
+        if (F.extra)
+            border_rows<ALIGNED>(p, sm, smbase, G, lane4);
+        G = N;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <bool ALIGNED>
+__global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
+    const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const uint32_t lane4 = (uint32_t)lane * 4u;
-    const Geo geo{p.pitch, p.w, p.band_rows, p.r0, p.h_total};
-    const StripedCorr scorr{sm + kSmCorr, lane4};
+    const int warp = tid >> 5;
     phase(0);
-
-#ifdef KOHLER_PHASES
-    const long long rb = (blockIdx.x + g_rot) % gridDim.x;  // debug: rotate ranges vs CTAs
-#else
     const long long rb = blockIdx.x;
-#endif
-    // balanced partition: the first cta_r ranges hold cta_q + 1 units
     const long long cs = rb * p.cta_q + (rb < p.cta_r ? rb : p.cta_r);
     const long long ce = cs + p.cta_q + (rb < p.cta_r ? 1 : 0);
 
@@ -384,51 +734,29 @@ __global__ void __launch_bounds__(kWideThreads, 1) wide_kernel(const WideParams 
     if (cs < ce) {
         int i_first = 0, i_last = 0;
         if (p.n > 1) {
-            i_first = (int)(cs / p.upi);
-            i_last = (int)((ce - 1) / p.upi);
+            i_first = (int)(cs / p.gpi);
+            i_last = (int)((ce - 1) / p.gpi);
         }
         for (int img = i_first; img <= i_last; ++img) {
-            const long long ibase = (long long)img * p.upi;
+            const long long ibase = (long long)img * p.gpi;
             const long long a = (cs > ibase ? cs : ibase) - ibase;
-            const long long b = (ce < ibase + p.upi ? ce : ibase + p.upi) - ibase;
+            const long long b = (ce < ibase + p.gpi ? ce : ibase + p.gpi) - ibase;
             const uint8_t* base = p.px + (size_t)img * p.image_stride;
-            // warp w walks a contiguous run of the CTA's sub-range [a, b),
-            // ping-ponging two register buffers one unit ahead
-            const int warp = tid >> 5;
-            const long long u0 = a + (b - a) * warp / 32;
-            int rem = (int)(a + (b - a) * (warp + 1) / 32 - u0);
-            const int aq = p.adv_q, ar = p.adv_r;
-            Cursor c0, c1;
-            unit_pos(p, u0, lane, c0.y, c0.seg);
-            Segment A, B;
-            A.rn = B.rn = 0;
-            if (rem > 0)
-                fetch<VEC>(geo, base, c0.y, c0.seg, A);
-            if (!zeroed) {
-                // overlap the first loads with clearing the histogram
-                zero_hist(sm, tid);
-                __syncthreads();
+            for (long long ea = a; ea < b; ea += p.epoch) {
+                const long long eb = ea + p.epoch < b ? ea + p.epoch : b;
+                const long long n = eb - ea;
+                const long long wa = ea + n * warp / kWalkWarps;
+                const long long wb = ea + n * (warp + 1) / kWalkWarps;
+                walk_range<ALIGNED>(p, sm, smbase, base, wa, wb, !zeroed);
+                warp_end();
                 zeroed = true;
-                phase(1);
+                __syncthreads();
+                if (eb < b) {
+                    for (int t = tid; t < 512; t += kWalkThreads)
+                        spill_w(sm, t);
+                    __syncthreads();
+                }
             }
-            c1 = c0;
-            c1.advance(p.nseg, aq, ar);
-            while (rem > 0) {
-                if (rem > 1)
-                    fetch<VEC>(geo, base, c1.y, c1.seg, B);
-                process<ALIGNED>(geo, sm, c0.y, c0.seg, lane4, A, scorr);
-                if (--rem == 0)
-                    break;
-                c0 = c1;
-                c0.advance(p.nseg, aq, ar);
-                if (rem > 1)
-                    fetch<VEC>(geo, base, c0.y, c0.seg, A);
-                process<ALIGNED>(geo, sm, c1.y, c1.seg, lane4, B, scorr);
-                --rem;
-                c1 = c0;
-                c1.advance(p.nseg, aq, ar);
-            }
-            __syncthreads();
             if (img == i_last) {
                 phase(2);
                 pdl_trigger();  // the next launch may start as SMs free up
@@ -827,7 +1155,9 @@ struct kohler_cuda_ctx {
     DevBuf img;      // staging for host images
     DevBuf out;      // staging for host outputs
     DevBuf curves;   // K5 curve scratch when the caller wants no curves
+    DevBuf stage;    // 16-byte aligned copy of unaligned device inputs for K1
     int last_launches = 0;
+    int last_grid = 0;  // grid of the last K1 launch (debug tools)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };
@@ -880,14 +1210,26 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
 {
     if (n == 0)
         return KOHLER_OK;
+    if (pitch >= (1ull << 31) / 64)
+        return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
     const int nseg = (w + 15) / 16;
-    const long long segs = (long long)band_rows * nseg;
-    const long long upi = (segs + 31) / 32;
-    const long long U = upi * n;
+    const int G_max = std::max(1, ctx->sm_count - 1);
+    // Rows per column walk: aim for ~2 groups of 32 walks per warp and keep
+    // the per-group prime row (one extra row load) amortised.
+    const long long tasks_target = (long long)G_max * kWalkWarps * 2 * 32;
+    const long long chunks_target = std::max(1ll, tasks_target / std::max(1, n) / nseg);
+    long long R = (band_rows + chunks_target - 1) / chunks_target;
+    // R = 2 (mod 4): a group is R + 2 ring positions, a multiple of the
+    // 4-slot ring, so every group starts at slot 0 (static register indexing)
+    R = std::min(30ll, std::max(6ll, R));
+    R += (6 - R % 4) % 4;
+    const long long chunks = (band_rows + R - 1) / R;
+    const long long T = chunks * nseg;
+    const long long gpi = (T + 31) / 32;
+    const long long U = gpi * n;
     // One CTA per SM, leaving one SM free: with programmatic dependent launch
     // the next launch's CTAs then never wait for this launch's serial tail.
-    long long G = (U + 63) / 64;
-    G = std::max(1ll, std::min<long long>(G, std::max(1, ctx->sm_count - 1)));
+    long long G = std::max(1ll, std::min<long long>(U, G_max));
     const int copies = n == 1 ? kAccCopiesSingle : 1;
     int rc = ctx->acc.ensure((size_t)n * copies * 512 * sizeof(unsigned long long), true);
     if (rc)
@@ -903,16 +1245,19 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     p.n = n;
     p.w = w;
     p.band_rows = band_rows;
+    p.buf_rows = band_rows + (r0 + band_rows < h_total ? 1 : 0);
     p.h_total = h_total;
     p.r0 = r0;
     p.nseg = nseg;
-    p.upi = upi;
-    p.total_units = U;
+    p.R = (int)R;
+    p.T = T;
+    p.gpi = gpi;
+    p.total_groups = U;
+    // a W lane word gets <= 16 * (R/2 + 1) events per group (its row parity + halo)
+    p.epoch = (int)std::max(1ll, (long long)kohler_walk::kMaxEventsPerWord / (16 * (R / 2 + 1)));
     p.acc = static_cast<unsigned long long*>(ctx->acc.p);
     p.copies = copies;
     p.tickets = static_cast<unsigned*>(ctx->tickets.p);
-    p.adv_q = 32 / nseg;
-    p.adv_r = 32 % nseg;
     p.cta_q = U / G;
     p.cta_r = U % G;
     p.seg_magic = nseg > 1 ? (unsigned long long)((((unsigned __int128)1) << 64) / (unsigned)nseg) + 1ull
@@ -930,21 +1275,39 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
 
     const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
                      (n == 1 || image_stride % 16 == 0);
+    if (!vec) {
+        // K1 reads 16-byte segments with cp.async: stage unaligned inputs
+        const size_t dpitch = round_up((size_t)w, 16);
+        const size_t dstride = dpitch * (size_t)p.buf_rows;
+        rc = ctx->stage.ensure(dstride * (size_t)n);
+        if (rc)
+            return rc;
+        uint8_t* d = static_cast<uint8_t*>(ctx->stage.p);
+        if (n == 1 || image_stride == pitch * (size_t)p.buf_rows) {
+            KC_CUDA(cudaMemcpy2DAsync(d, dpitch, px, pitch, (size_t)w, (size_t)p.buf_rows * n,
+                                      cudaMemcpyDeviceToDevice, stream));
+        } else {
+            for (int i = 0; i < n; ++i)
+                KC_CUDA(cudaMemcpy2DAsync(d + dstride * i, dpitch, px + image_stride * i, pitch,
+                                          (size_t)w, (size_t)p.buf_rows, cudaMemcpyDeviceToDevice,
+                                          stream));
+        }
+        p.px = d;
+        p.pitch = dpitch;
+        p.image_stride = dstride;
+    }
     // the smem opt-in is per device; remember it per context
     if (!ctx->wide_attr_set) {
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true, true>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<true, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(wide_kernel<false, false>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         ctx->wide_attr_set = true;
     }
+    ctx->last_grid = (int)G;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(kWideThreads);
+    cfg.blockDim = dim3(kWalkThreads);
     cfg.dynamicSmemBytes = kSmWideBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -952,15 +1315,10 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const bool aligned = w % 16 == 0;
-    if (vec && aligned)
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true, true>, p));
-    else if (vec)
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<true, false>, p));
-    else if (aligned)
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false, true>, p));
+    if (w % 16 == 0)
+        KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<true>, p));
     else
-        KC_CUDA(cudaLaunchKernelEx(&cfg, wide_kernel<false, false>, p));
+        KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<false>, p));
     KC_CUDA(cudaGetLastError());
     ctx->last_launches += 1;
     return KOHLER_OK;
@@ -1203,6 +1561,7 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         ctx->img.release();
         ctx->out.release();
         ctx->curves.release();
+        ctx->stage.release();
         cudaStreamDestroy(ctx->stream);
     }
     delete ctx;

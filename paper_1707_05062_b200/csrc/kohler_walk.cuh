@@ -1,0 +1,205 @@
+// kohler_walk.cuh — K1 accumulation, "three events per pixel".
+//
+// Every lane walks DOWN a column of one 16-pixel segment, so each pixel's
+// four neighbour relations are available without re-reading anything:
+// the right pair (within the lane's registers + one neighbour byte), the
+// down pair (the next row, loaded ahead) and, carried from the previous
+// row, the up pair.  Per pixel x with value v it emits
+//
+//   W[v]      += B(x) << 16 | 1          (packed: sign sum, pixel count)
+//   Hs[v + r] += 1                       (right pair midpoint event)
+//   Hs[v + d] += 1                       (down pair midpoint event)
+//
+// with B(x) = sum over the 4 neighbour slots of (1 + sign(n - v)) in [0, 8]
+// (a missing / fake neighbour counts as an equal one).  That is 3 shared
+// atomics per pixel instead of the 5 of the marginal-histogram form
+// (hist + H_hi + H_s per pair), which is what bounds this kernel.
+//
+// Reconstruction (SURVEY.md Appendix A restated on these counters): with
+// hist = sum of the low fields, Bs = sum of the high fields, P = 4 hist - corr,
+//     card'[v] = Bs[v] - 4 hist[v]          (= sum_x sum_n sign(n - v): +1 at lo, -1 at hi)
+//     sum''[u] = P[u-1] - Hs[2u-3] - 2 Hs[2u-2] - Hs[2u-1]
+// because the tent min(hi - t, t - lo) (proj/src/kernels/pair_tent.hpp:12-18)
+// has second difference +1 at lo+1 and hi+1 and -1 at floor(s/2)+1,
+// ceil(s/2)+1.  `corr` fixes P at borders: P must count, for every pixel,
+// its incidences among the EMITTED pairs, with an emitted equal "fake" pair
+// counted twice.  Row start / first band row (pair missing or not owned):
+// corr +1.  Row end / last image row (fake equal pair emitted): corr -1.
+// Halo pixel (one owned up pair, emitted as a W event): corr +3.
+//
+// The per-pair sign step q(a -> b) = 1 + sign(b - a) is computed two pairs
+// at a time in 16-bit SIMD lanes (qstep below).  Only differences of q enter
+// B, so B needs no per-pair offsets.  The work is split between the integer
+// ALU pipe and the FMA pipe (IMAD), which on sm_100 each retire half a warp
+// instruction per cycle per scheduler; the ALU pipe, not the shared atomics,
+// is what bounds this loop.
+//
+// Shared memory (lane-striped: lane L only touches bank L, so every warp-wide
+// update is conflict free for any data):
+//   rows of 256 B, word (row, half, lane) at row*256 + half*128 + lane*4
+//   half 0, rows 0..510 : Hs[s];  row 511: dummy (neutralised events)
+//   half 1, rows 0..255 : W copy 0 (even rows);  rows 256..511: W copy 1 (odd rows)
+//   + 32 KiB corr[v][lane] at kCorr + v*128 + lane*4 (int)
+// A pixel's W address is A = (v << 8) | lane*4 (one PRMT); a pair's Hs
+// address is A_a + A_b - lane*4 = (a + b) << 8 | lane*4 (one IADD3).
+#pragma once
+
+#include <cstdint>
+
+namespace kohler_walk {
+
+constexpr uint32_t kHistBytes = 512u * 256u;       // Hs / dummy / W0 / W1
+constexpr uint32_t kOffW0 = 128;
+constexpr uint32_t kOffW1 = 65536 + 128;
+constexpr uint32_t kCorr = kHistBytes;             // int[256][32]
+constexpr uint32_t kCorrBytes = 32768;
+constexpr uint32_t kDummy = 511u << 8;
+// W word = Bsum << 16 | hist.  A W lane word takes at most this many pixel
+// events between spills, so hist and Bsum <= 8 * it fit 16 bits each.
+constexpr int kMaxEventsPerWord = 8191;
+constexpr uint32_t kTo = 0x02020202u;              // unpack fill: lanes b + 512 ("to" form)
+constexpr uint32_t kNeutral = 0x00010001u;         // q of an equal pair, both lanes
+
+struct Row {  // one prefetched 16-pixel row segment + its neighbour bytes
+    uint32_t w[4];
+    uint32_t ln, rn;
+};
+
+struct Car {  // a row segment in the form the accumulation uses
+    uint32_t A[16];      // (v << 8) | lane*4 per pixel
+    uint32_t e[4], o[4]; // 16-bit lanes b + 512: e[j] = (b4j, b4j+2), o[j] = (b4j+1, b4j+3)
+    uint32_t ue[4], uo[4];  // q(up -> this) per pixel, same lane layout
+    uint32_t ln, rn;     // left / right neighbour byte (fixed up at borders)
+};
+
+// The sign step q(from -> to) = 1 + sign(to - from) in {0, 1, 2} per 16-bit
+// lane, by ONE VIADDMNMX.S16x2.RELU: relu(min(to + nf, 2)) lanewise.
+// Unpacked lanes are kept in "to" form x'' = b + 512 (the unpack PRMT's fill
+// byte); a "from" operand is nf = 1 - x'' per lane, made by one subtract from
+// 0x00020001: the low lane always borrows exactly once (x'' >= 512), which
+// the high half of the constant pre-pays.  to + nf = to - from + 1.
+__device__ __forceinline__ uint32_t qfrom(uint32_t to_form)
+{
+    return 0x00020001u - to_form;
+}
+
+__device__ __forceinline__ uint32_t qstep(uint32_t nf, uint32_t to_form)
+{
+    return __vimin_s16x2_relu(__vadd2(to_form, nf), 0x00020002u);
+}
+
+__device__ __forceinline__ void red_inc(uint32_t saddr)
+{
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr));
+}
+
+// Pair event at shared address a + b + c (kept opaque to the front end so the
+// two adds fuse into one IADD3 instead of being re-associated around
+// common sub-expressions).
+__device__ __forceinline__ void red_inc3(uint32_t a, uint32_t b, uint32_t c)
+{
+    asm volatile("{\n\t.reg .u32 t;\n\tadd.u32 t, %0, %1;\n\tadd.u32 t, t, %2;\n\t"
+                 "red.shared.add.u32 [t], 1;\n\t}" ::"r"(a), "r"(b), "r"(c));
+}
+
+__device__ __forceinline__ void red_add(uint32_t saddr, uint32_t v)
+{
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
+}
+
+// corr word of the pixel whose W address is A
+__device__ __forceinline__ uint32_t corr_addr(uint32_t smbase, uint32_t A, uint32_t lane4)
+{
+    return smbase + kCorr + ((A >> 8) << 7) + lane4;
+}
+
+// Unpack a loaded row into Y.  The loads already applied the border rule for
+// aligned segments (a row start's left neighbour and a row end's right
+// neighbour are the pixel itself: equal => neutral); a ragged segment (row
+// end inside it, index e < 15) gets its bytes past the row end replaced by
+// the last real pixel, which is also its right neighbour.
+template <bool ALIGNED>
+__device__ __forceinline__ void absorb(Car& Y, const Row& r0, uint32_t lane4, int e)
+{
+    Row r = r0;
+    if (!ALIGNED && e < 15) {
+        const uint32_t wd = e < 4 ? r.w[0] : e < 8 ? r.w[1] : e < 12 ? r.w[2] : r.w[3];
+        const uint32_t v = (wd >> (8 * (e & 3))) & 0xFFu;
+        const uint32_t vvvv = v * 0x01010101u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int keep = e - 4 * j + 1;  // bytes of word j to keep
+            if (keep <= 0)
+                r.w[j] = vvvv;
+            else if (keep < 4) {
+                const uint32_t m = 0xFFFFFFFFu << (8 * keep);
+                r.w[j] = (r.w[j] & ~m) | (vvvv & m);
+            }
+        }
+        r.rn = v;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        Y.e[j] = __byte_perm(r.w[j], kTo, 0x4240);
+        Y.o[j] = __byte_perm(r.w[j], kTo, 0x4341);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            Y.A[4 * j + k] = __byte_perm(r.w[j], lane4, 0x5504 | (k << 4));
+    }
+    Y.ln = r.ln;
+    Y.rn = r.rn;
+}
+
+// q of the four pair families of the current row X against the down row
+// (De, Do).  qre/qro: right pairs of even/odd pixels; qde/qdo: down pairs.
+__device__ __forceinline__ void pair_q(const Car& X, const uint32_t (&De)[4],
+                                       const uint32_t (&Do)[4], uint32_t (&qre)[4],
+                                       uint32_t (&qro)[4], uint32_t (&qde)[4], uint32_t (&qdo)[4])
+{
+    const uint32_t rn_to = X.rn | 0x0200u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t ro = __byte_perm(X.e[j], j < 3 ? X.e[j + 1] : rn_to, 0x5432);
+        const uint32_t fe = qfrom(X.e[j]), fo = qfrom(X.o[j]);
+        qre[j] = qstep(fe, X.o[j]);
+        qro[j] = qstep(fo, ro);
+        qde[j] = qstep(fe, De[j]);
+        qdo[j] = qstep(fo, Do[j]);
+    }
+}
+
+// B(x) for the 16 pixels, exact in 16-bit lanes: Be[j] = (B(4j), B(4j+2)),
+// Bo[j] = (B(4j+1), B(4j+3)).
+__device__ __forceinline__ void b_terms(const Car& X, const uint32_t (&qre)[4],
+                                        const uint32_t (&qro)[4], const uint32_t (&qde)[4],
+                                        const uint32_t (&qdo)[4], uint32_t (&Be)[4],
+                                        uint32_t (&Bo)[4])
+{
+    // low lane: q(left neighbour -> b0), nf = 1 - (ln + 512)
+    const uint32_t qL = qstep(0xFFFFFE01u - X.ln, X.e[0]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t qrl = j == 0 ? __byte_perm(qL, qro[0], 0x5410)
+                                    : __byte_perm(qro[j - 1], qro[j], 0x5432);
+        Be[j] = 0x00040004u + qre[j] - qrl + qde[j] - X.ue[j];
+        Bo[j] = 0x00040004u + qro[j] - qre[j] + qdo[j] - X.uo[j];
+    }
+}
+
+// Increment of pixel i's W word, B(i) << 16 | 1: the low lane by one IMAD
+// (the high lane shifts out), the high lane by one LOP3.
+__device__ __forceinline__ uint32_t inc_of(uint32_t lanes, int hi)
+{
+    if (!hi)
+        return lanes * 65536u + 1u;
+    uint32_t r;
+    asm("lop3.b32 %0, %1, 0xFFFF0000, %2, 0xEA;" : "=r"(r) : "r"(lanes), "r"(1u));  // (a & b) | c
+    return r;
+}
+
+__device__ __forceinline__ uint32_t b_of(const uint32_t (&Be)[4], const uint32_t (&Bo)[4], int i)
+{
+    return inc_of((i & 1) ? Bo[i >> 2] : Be[i >> 2], i & 2);
+}
+
+} // namespace kohler_walk

@@ -57,8 +57,7 @@ int main(int argc, char** argv)
     printf("isolated launch (event): median %.2f us\n", tot[reps / 2]);
     static unsigned long long ph[2048][8];
     cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
-    const long long U = ((long long)h * ((w + 15) / 16) + 31) / 32;
-    int G = (int)std::max(1ll, std::min<long long>((U + 63) / 64, ctx->sm_count - 1));
+    const int G = ctx->last_grid;
     printf("grid %d CTAs\n", G);
     unsigned long long t0 = ~0ull, tend = 0;
     for (int c = 0; c < G; ++c) { t0 = std::min(t0, ph[c][0]); tend = std::max(tend, ph[c][7]); }
@@ -88,6 +87,22 @@ int main(int argc, char** argv)
         printf("\nfastest CTAs (cta/sm): ");
         for (int i = 0; i < std::min(8, (int)v.size()); ++i) printf("%d/%u ", v[i].second, smid[v[i].second]);
         printf("\n");
+    }
+    {
+        static unsigned long long we[2048][32];
+        cudaMemcpyFromSymbol(we, g_wend, sizeof(we));
+        const int nw = kWalkWarps;
+        double spread = 0, avgw = 0;
+        for (int c = 0; c < G; ++c) {
+            double mn = 1e18, mx = 0;
+            for (int w2 = 0; w2 < nw; ++w2) {
+                const double t = (we[c][w2] - ph[c][1]) / 1e3;
+                mn = std::min(mn, t); mx = std::max(mx, t);
+                avgw += t;
+            }
+            spread += mx - mn;
+        }
+        printf("warp walk end (us after zeroing): avg %.2f, avg per-CTA spread max-min %.2f\n", avgw / (G * nw), spread / G);
     }
     if (lastCta >= 0)
         printf("tail CTA %d: flush done %.2f, acc read %.2f, scans+mean %.2f, select %.2f, end %.2f us\n", lastCta,
