@@ -50,10 +50,11 @@ struct WideParams {
     int R;          // rows per column walk (even)
     long long T;    // walk tasks per image (S * ceil(band_rows / R))
     long long gpi;  // 32-lane groups per image
-    long long total_groups;
-    int epoch;      // max groups between W spills (kohler_walk::kMaxEventsPerWord)
+    long long upi;  // units per image: gpi * R (unit = one row of a group's 32 walks)
+    long long total_units;
+    int epoch;      // max units between W spills (kohler_walk::kMaxEventsPerWord)
     unsigned long long seg_magic;  // floor(2^64 / nseg) + 1 (nseg > 1)
-    long long cta_q, cta_r;        // total_groups = cta_q * G + cta_r
+    long long cta_q, cta_r;        // total_units = cta_q * G + cta_r
     unsigned long long* acc;  // [n][copies][512]
     int copies;
     unsigned* tickets;  // [n]
@@ -296,8 +297,8 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
         wacc[t] = 0;
     __shared__ int s_last;
     if (tid == 0) {
-        const long long first = cta_of_unit((long long)img * p.gpi, p.cta_q, p.cta_r);
-        const long long last = cta_of_unit((long long)(img + 1) * p.gpi - 1, p.cta_q, p.cta_r);
+        const long long first = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
+        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, p.cta_q, p.cta_r);
         const unsigned expected = (unsigned)(last - first + 1);
         const unsigned prev = atomicAdd(p.tickets + img, 1u);
         s_last = (prev + 1 == expected);
@@ -411,8 +412,8 @@ __device__ __forceinline__ void process(const Geo& p, unsigned char* sm, int y, 
 // ---------------------------------------------------------------------------
 struct LaneGeo {
     const uint8_t* p;  // row y0 - 1, column x0 (dereferenced only for valid rows)
-    const uint8_t* pl; // p - 1 if the segment has a left neighbour, else p
-    const uint8_t* pr; // p + 16 if the segment has a right neighbour, else p + 15
+    uint32_t pad;      // lane 0 / 31: also copy the 16 bytes left / right (neighbour exists)
+    int pd;            // -16 (lane 0) or +16
     int x0;
     int y0;            // first own row (band-relative)
     int nrows;         // own rows of the walk (0: no task)
@@ -444,8 +445,8 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
         L.jcl = 0;
     }
     L.p = base + ((long long)L.y0 - 1) * (long long)p.pitch + L.x0;
-    L.pl = L.p - (L.x0 > 0 ? 1 : 0);
-    L.pr = L.p + (L.e > 15 ? 16 : 15);
+    L.pd = lane == 0 ? -16 : 16;
+    L.pad = ((lane == 0) & (L.x0 > 0)) | ((lane == 31) & (L.e > 15)) ? 1u : 0u;
     return L;
 }
 
@@ -453,20 +454,16 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
 // (shared address of this lane's 16-byte segment in the slot): the segment,
 // from a clamped valid row, and for lane 0 / lane 31 the 16 bytes left /
 // right of it where that neighbour exists.  One cp.async group per position.
-__device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitch, uint32_t dst,
-                                         int lane)
+__device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitch, uint32_t dst)
 {
     const uint32_t off = (uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
-    // lane 0 / 31 also copy the 16 bytes left / right of the segment (if the
-    // neighbour exists): predicated, no branch
-    const int d = lane == 0 ? -16 : 16;
-    const uint32_t pad = ((lane == 0 && L.x0 > 0) || (lane == 31 && L.e > 15)) ? 1u : 0u;
+    const uint8_t* src = L.p + off;
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
         "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
         "@p cp.async.cg.shared.global [%3], [%4], 16;\n\t"
         "cp.async.commit_group;\n\t}" ::"r"(dst),
-        "l"(L.p + off), "r"(pad), "r"(dst + d), "l"(L.p + off + d)
+        "l"(src), "r"(L.pad), "r"(dst + L.pd), "l"(src + L.pd)
         : "memory");
 }
 
@@ -487,9 +484,8 @@ __device__ __forceinline__ void read_row(kohler_walk::Row& r, uint32_t seg, uint
 
 // Per-group, warp-uniform flags.
 struct GroupFlags {
-    bool edge;       // some lane is at a row start or row end (corr terms)
-    bool ragged;     // some lane's segment runs past the row end (garbage bytes)
-    unsigned extra;  // bit j: some lane's row at position j needs border terms
+    bool edge;    // some lane is at a row start or row end (corr terms)
+    bool ragged;  // some lane's segment runs past the row end (garbage bytes)
 };
 
 __device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const LaneGeo& L, bool aligned)
@@ -498,15 +494,6 @@ __device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const Lan
     const bool act = L.nrows > 0;
     f.edge = __any_sync(0xFFFFFFFFu, act && (L.x0 == 0 || L.e <= 15));
     f.ragged = !aligned && __any_sync(0xFFFFFFFFu, act && L.e < 15);
-    unsigned m = 0;
-    if (act) {
-        // position j processes band row y0 + j - 2
-        if (L.y0 == 0)
-            m |= 1u << 2;  // band first row: up pair missing / not owned
-        if (L.y0 + L.nrows == p.band_rows)
-            m |= 1u << (L.nrows + 1);  // band last row: last image row or halo
-    }
-    f.extra = __reduce_or_sync(0xFFFFFFFFu, m);
     return f;
 }
 
@@ -519,10 +506,12 @@ __device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const Lan
 //                         event B = 4 + sign(c - d) = 5 - q(c -> d), corr +3
 template <bool ALIGNED>
 __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm, uint32_t smbase,
-                                         const LaneGeo& G, uint32_t lane4)
+                                         const LaneGeo& G, int r0, int r1, uint32_t lane4)
 {
     using namespace kohler_walk;
-    if (G.nrows <= 0)
+    // this lane walked rows y0 + [r0, r1) of its column (clipped to its own rows)
+    r1 = min(r1, G.nrows);
+    if (r0 >= r1)
         return;
     const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
     auto load16 = [&](int y, uint32_t (&w)[4]) {
@@ -537,13 +526,13 @@ __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm,
         }
     };
     auto byte = [](const uint32_t (&w)[4], int i) { return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu; };
-    if (G.y0 == 0) {
+    if (G.y0 + r0 == 0) {
         uint32_t w[4];
         load16(0, w);
         for (int i = 0; i < nreal; ++i)
             red_add(smbase + kCorr + (byte(w, i) << 7) + lane4, 1u);
     }
-    const int ylast = G.y0 + G.nrows - 1;
+    const int ylast = G.y0 + r1 - 1;
     if (ylast == p.band_rows - 1) {
         uint32_t c[4];
         load16(ylast, c);
@@ -563,10 +552,17 @@ __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm,
     }
 }
 
+// A warp walks the contiguous run [ua, ub) of "units" of one image: unit u =
+// row u % R of the 32 column walks of group u / R.  The run is a sequence of
+// segments (one per group touched); a segment of L rows is L + 2 ring
+// positions: row r0 - 1 (absorbed), row r0 (prime: q of the up pairs), then
+// one position per row.  Rows stream through the warp's 4-slot shared ring,
+// prefetched 3 positions ahead across segment boundaries.  The W copy
+// alternates with the position parity (bounds each copy's events).
 template <bool ALIGNED>
 __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
-                                           uint32_t smbase, const uint8_t* base, long long ga,
-                                           long long gb, bool zero_first)
+                                           uint32_t smbase, const uint8_t* base, long long ua,
+                                           long long ub, bool zero_first)
 {
     using namespace kohler_walk;
     const int lane = threadIdx.x & 31;
@@ -574,19 +570,26 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     const uint32_t lane4 = (uint32_t)lane * 4u;
     const uint32_t kneg = smbase - lane4;
     const uint32_t dummy = smbase + kDummy + lane4;
-    const int P = p.R + 2;  // ring positions per group (rows y0-1 .. y0+R), P % 4 == 0
+    const int R = p.R;
     const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
-    const bool any = ga < gb;
+    const bool any = ua < ub;
     // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
     const uint32_t seg0 = smbase + kSmRing + (uint32_t)warp * (kRingSlots * kSlotBytes) + 16u +
                           (uint32_t)lane * 16u;
 
+    // current segment: group g, rows [r0, r1) of its walks; next segment
+    long long g = 0;
+    int r0 = 0, r1 = 0;
     LaneGeo G{};
     if (any) {
-        G = lane_geo(p, base, ga, lane);
-        fetch_row(G, 0, pitch, seg0, lane);
-        fetch_row(G, 1, pitch, seg0 + kSlotBytes, lane);
-        fetch_row(G, 2, pitch, seg0 + 2 * kSlotBytes, lane);
+        g = ua / R;
+        r0 = (int)(ua - g * R);
+        r1 = (int)(ub - g * R < (long long)R ? (int)(ub - g * R) : R);
+        G = lane_geo(p, base, g, lane);
+        // positions 0, 1, 2 of the first segment (rows r0 - 1, r0, r0 + 1 of the walk)
+        fetch_row(G, r0, pitch, seg0);
+        fetch_row(G, r0 + 1, pitch, seg0 + kSlotBytes);
+        fetch_row(G, r0 + 2, pitch, seg0 + 2 * kSlotBytes);
     }
     if (zero_first) {
         // clear the counters while the first rows are in flight
@@ -600,41 +603,46 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         return;
 
     Car X, Y;
-    for (long long g = ga; g < gb; ++g) {
-        const bool has_next = g + 1 < gb;
-        LaneGeo N = G;  // next group's geometry, computed before the last block
+    uint32_t pos = 0;  // ring position of the segment's position 0 (mod 4 picks the slot)
+    for (;;) {
+        const int L = r1 - r0;
+        const int P = L + 2;
+        const long long gn = g + 1;
+        const bool has_next = gn * R < ub;
+        const int nr1 = has_next ? (int)(ub - gn * R < (long long)R ? (int)(ub - gn * R) : R) : 0;
+        const LaneGeo N = has_next ? lane_geo(p, base, gn, lane) : G;
         const GroupFlags F = group_flags(p, G, ALIGNED);
         const bool row_start = G.x0 == 0, row_end = G.e <= 15;
         const uint32_t offl = G.x0 > 0 ? 0xFFFFFFFFu : 0u;  // left neighbour byte
         const uint32_t offr = G.e > 15 ? 16u : 15u;         // right neighbour byte
 
-        // One ring position j (slot s = j & 3): prefetch position j + 3 (of
-        // this group or, past its end, of the next), absorb row j into D and
-        // process row j - 1 (C) against it.  WC: W copy of C's row parity.
-        auto step = [&](Car& D, Car& C, int j, auto slot, auto kind, auto wc) {
-            constexpr int S = decltype(slot)::value;
-            constexpr int KIND = decltype(kind)::value;  // 0 absorb, 1 prime, 2 process, 3 process + cross
+        // One ring position j: prefetch position j + 3 (of this segment or,
+        // past its end, of the next), absorb row r0 - 1 + j into D and
+        // process row r0 - 2 + j (C) against it.
+        auto step = [&](Car& D, Car& C, int j, auto kind, auto wc, auto cross) {
+            constexpr int KIND = decltype(kind)::value;  // 0 absorb, 1 prime, 2 process
+            constexpr bool CROSS = decltype(cross)::value;  // prefetch may cross into the next segment
             constexpr int WC = decltype(wc)::value;
             constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
-            constexpr uint32_t kPref = ((S + 3) & 3) * kSlotBytes;
-            // slot S was committed 3 groups ago; <= 2 younger groups may pend
+            const uint32_t q = pos + (uint32_t)j;
+            // slot q & 3 was committed 3 groups ago; <= 2 younger groups may pend
             asm volatile("cp.async.wait_group 2;" ::: "memory");
+            // all lanes' copies into slot q & 3 are visible, and all lanes have
+            // read slot (q - 1) & 3 (the previous position), which is refilled now
             __syncwarp();
+            const uint32_t pref = seg0 + ((q + 3u) & 3u) * kSlotBytes;
+            if (!CROSS || j + 3 < P)
+                fetch_row(G, r0 + j + 3, pitch, pref);
+            else if (has_next)
+                fetch_row(N, j + 3 - P, pitch, pref);
+            else
+                asm volatile("cp.async.commit_group;" ::: "memory");
             Row r;
-            read_row(r, seg0 + S * kSlotBytes, offl, offr);
-            __syncwarp();  // every lane has read slot S before anyone refills it
-            if (KIND == 3 && j + 3 >= P) {
-                if (has_next)
-                    fetch_row(N, j + 3 - P, pitch, seg0 + kPref, lane);
-                else
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-            } else {
-                fetch_row(G, j + 3, pitch, seg0 + kPref, lane);
-            }
+            read_row(r, seg0 + (q & 3u) * kSlotBytes, offl, offr);
             absorb<ALIGNED>(D, r, lane4, G.e);
             if (KIND == 1) {
-                // prime: q(up -> row y0) from row y0 - 1 (neutral at the band's first row)
-                const bool has_up = G.y0 > 0;
+                // prime: q(up -> row r0) from row r0 - 1 (neutral at the band's first row)
+                const bool has_up = G.y0 + r0 > 0;
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
                     D.ue[jj] = has_up ? qstep(qfrom(C.e[jj]), D.e[jj]) : kNeutral;
@@ -643,7 +651,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             }
             if (KIND < 2)
                 return;
-            const bool live = j - 2 < G.nrows;
+            const bool live = r0 + j - 2 < G.nrows;
             uint32_t qre[4], qro[4], qde[4], qdo[4], Be[4], Bo[4];
             pair_q(C, D.e, D.o, qre, qro, qde, qdo);
             b_terms(C, qre, qro, qde, qdo, Be, Bo);
@@ -686,32 +694,40 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         using K0 = std::integral_constant<int, 0>;
         using K1 = std::integral_constant<int, 1>;
         using K2 = std::integral_constant<int, 2>;
-        using K3 = std::integral_constant<int, 3>;
-        using S0 = std::integral_constant<int, 0>;
-        using S1 = std::integral_constant<int, 1>;
-        using S2 = std::integral_constant<int, 2>;
-        using S3 = std::integral_constant<int, 3>;
-        // positions 0..3: absorb row y0-1, prime row y0, process rows y0, y0+1
-        // (W copy = parity of the processed row = parity of j, y0 even)
-        step(X, Y, 0, S0{}, K0{}, S0{});
-        step(Y, X, 1, S1{}, K1{}, S1{});
-        step(X, Y, 2, S2{}, K2{}, S0{});
-        step(Y, X, 3, S3{}, K2{}, S1{});
-        int j = 4;
-        for (; j < P - 4; j += 4) {
-            step(X, Y, j, S0{}, K2{}, S0{});
-            step(Y, X, j + 1, S1{}, K2{}, S1{});
-            step(X, Y, j + 2, S2{}, K2{}, S0{});
-            step(Y, X, j + 3, S3{}, K2{}, S1{});
+        using W0 = std::integral_constant<int, 0>;
+        using W1 = std::integral_constant<int, 1>;
+        using NC = std::false_type;
+        using CR = std::true_type;
+        // positions whose prefetch stays in this segment: j + 3 < P
+        if (P > 4) {
+            step(X, Y, 0, K0{}, W0{}, NC{});
+            step(Y, X, 1, K1{}, W1{}, NC{});
+        } else {
+            step(X, Y, 0, K0{}, W0{}, CR{});
+            step(Y, X, 1, K1{}, W1{}, CR{});
         }
-        if (has_next)
-            N = lane_geo(p, base, g + 1, lane);
-        step(X, Y, j, S0{}, K3{}, S0{});
-        step(Y, X, j + 1, S1{}, K3{}, S1{});
-        step(X, Y, j + 2, S2{}, K3{}, S0{});
-        step(Y, X, j + 3, S3{}, K3{}, S1{});
-        if (F.extra)
-            border_rows<ALIGNED>(p, sm, smbase, G, lane4);
+        int j = 2;
+        for (; j + 4 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, NC{});
+            step(Y, X, j + 1, K2{}, W1{}, NC{});
+        }
+        for (; j + 1 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, CR{});
+            step(Y, X, j + 1, K2{}, W1{}, CR{});
+        }
+        if (j < P)
+            step(X, Y, j, K2{}, W0{}, CR{});
+        const bool border = __any_sync(0xFFFFFFFFu, G.nrows > 0 && r0 < min(r1, G.nrows) &&
+                                                          ((G.y0 + r0 == 0) ||
+                                                           (G.y0 + min(r1, G.nrows) == p.band_rows)));
+        if (border)
+            border_rows<ALIGNED>(p, sm, smbase, G, r0, r1, lane4);
+        if (!has_next)
+            break;
+        pos += (uint32_t)P;
+        g = gn;
+        r0 = 0;
+        r1 = nr1;
         G = N;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -734,13 +750,13 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
     if (cs < ce) {
         int i_first = 0, i_last = 0;
         if (p.n > 1) {
-            i_first = (int)(cs / p.gpi);
-            i_last = (int)((ce - 1) / p.gpi);
+            i_first = (int)(cs / p.upi);
+            i_last = (int)((ce - 1) / p.upi);
         }
         for (int img = i_first; img <= i_last; ++img) {
-            const long long ibase = (long long)img * p.gpi;
+            const long long ibase = (long long)img * p.upi;
             const long long a = (cs > ibase ? cs : ibase) - ibase;
-            const long long b = (ce < ibase + p.gpi ? ce : ibase + p.gpi) - ibase;
+            const long long b = (ce < ibase + p.upi ? ce : ibase + p.upi) - ibase;
             const uint8_t* base = p.px + (size_t)img * p.image_stride;
             for (long long ea = a; ea < b; ea += p.epoch) {
                 const long long eb = ea + p.epoch < b ? ea + p.epoch : b;
@@ -1214,22 +1230,31 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
     const int nseg = (w + 15) / 16;
     const int G_max = std::max(1, ctx->sm_count - 1);
-    // Rows per column walk: aim for ~2 groups of 32 walks per warp and keep
-    // the per-group prime row (one extra row load) amortised.
-    const long long tasks_target = (long long)G_max * kWalkWarps * 2 * 32;
-    const long long chunks_target = std::max(1ll, tasks_target / std::max(1, n) / nseg);
-    long long R = (band_rows + chunks_target - 1) / chunks_target;
-    // R = 2 (mod 4): a group is R + 2 ring positions, a multiple of the
-    // 4-slot ring, so every group starts at slot 0 (static register indexing)
-    R = std::min(30ll, std::max(6ll, R));
-    R += (6 - R % 4) % 4;
+    // Rows per column walk R: a walk's rows past the band end still cost
+    // their steps, so prefer R dividing the band height; longer walks
+    // amortise the per-segment prime row.
+    long long R = 64;
+    {
+        double best = 1e30;
+        for (long long r = 16; r <= 64; ++r) {
+            const long long ch = (band_rows + r - 1) / r;
+            const double waste = (double)(ch * r - band_rows) / band_rows + 0.5 / r;
+            if (waste < best - 1e-12) {
+                best = waste;
+                R = r;
+            }
+        }
+        R = std::min<long long>(R, std::max(1, band_rows));
+    }
     const long long chunks = (band_rows + R - 1) / R;
     const long long T = chunks * nseg;
     const long long gpi = (T + 31) / 32;
-    const long long U = gpi * n;
+    const long long upi = gpi * R;
+    const long long U = upi * n;
     // One CTA per SM, leaving one SM free: with programmatic dependent launch
     // the next launch's CTAs then never wait for this launch's serial tail.
-    long long G = std::max(1ll, std::min<long long>(U, G_max));
+    // Small jobs: at least ~4 rows per warp.
+    long long G = std::max(1ll, std::min<long long>((U + 4 * kWalkWarps - 1) / (4 * kWalkWarps), G_max));
     const int copies = n == 1 ? kAccCopiesSingle : 1;
     int rc = ctx->acc.ensure((size_t)n * copies * 512 * sizeof(unsigned long long), true);
     if (rc)
@@ -1252,9 +1277,16 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     p.R = (int)R;
     p.T = T;
     p.gpi = gpi;
-    p.total_groups = U;
-    // a W lane word gets <= 16 * (R/2 + 1) events per group (its row parity + halo)
-    p.epoch = (int)std::max(1ll, (long long)kohler_walk::kMaxEventsPerWord / (16 * (R / 2 + 1)));
+    p.upi = upi;
+    p.total_units = U;
+    // Events into one W lane word per epoch of E units (rows), split over
+    // the warps in contiguous runs of k_w segments (k_w <= units_w / R + 2):
+    // copy 0 takes ceil(L/2) rows per segment plus <= 1 halo row per
+    // segment, 16 pixels each: <= 16 (E/2 + 1.5 (E/R + 2 W)) <= kMaxEvents.
+    {
+        const double cap = (double)kohler_walk::kMaxEventsPerWord / 16.0 - 3.0 * kWalkWarps;
+        p.epoch = (int)std::max(1.0, std::floor(cap / (0.5 + 1.5 / (double)R)));
+    }
     p.acc = static_cast<unsigned long long*>(ctx->acc.p);
     p.copies = copies;
     p.tickets = static_cast<unsigned*>(ctx->tickets.p);
