@@ -78,24 +78,34 @@ constexpr int kWalkWarps = kWalkThreads / 32;
 
 // Shared-memory map of K1 (dynamic), after the striped counters and corr
 // (kohler_walk.cuh).
-constexpr uint32_t kSmWacc = kohler_walk::kCorr + kohler_walk::kCorrBytes;  // u64 [2 copies][2 fields][256]
-constexpr uint32_t kSmHsTot = kSmWacc + 8192;        // u64[512]
-constexpr uint32_t kSmCorrTot = kSmHsTot + 4096;     // int[256]
+// Shared-memory map of K1 (dynamic).  The striped counter block (128 KiB,
+// kohler_walk.cuh) sits at the fixed shared-window address kHistAbs, so every
+// counter address is "register + compile-time immediate" (no base register
+// in the hot loop); everything else lives in the gap below it, at offsets
+// from the dynamic base.
+constexpr uint32_t kHistAbs = 0x10000;
 // Row ring of the column walks (cp.async destination): per warp kRingSlots
 // slots of 32 lane segments + a 16-byte pad on each side.  Idle during the
 // flush, so the reconstruction / selection scratch aliases it.
 constexpr int kRingSlots = 4;
 constexpr uint32_t kSlotBytes = 16 + 32 * 16 + 16;
-constexpr uint32_t kSmRing = kSmCorrTot + 1024;
+constexpr uint32_t kSmRing = 0;
 constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlotBytes;
+constexpr uint32_t kSmWacc = kSmRing + kRingBytes;   // u64 [2 copies][2 fields][256]
+constexpr uint32_t kSmHsTot = kSmWacc + 8192;        // u64[512]
+constexpr uint32_t kSmCorrTot = kSmHsTot + 4096;     // int[256]
+constexpr uint32_t kSmCorr = kSmCorrTot + 1024;      // int[256] border terms (corr)
+constexpr uint32_t kSmMiscEnd = kSmCorr + 1024;
 constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
 constexpr uint32_t kSmCurve = kSmVal + 4096;         // u64 sum[256], card[256]
 constexpr uint32_t kSmMean = kSmCurve + 4096;        // f64[256]
 constexpr uint32_t kSmDef = kSmMean + 2048;          // u8[256]
 constexpr uint32_t kSmScratch = kSmDef + 256;        // block_select256 scratch
 constexpr uint32_t kSmFinishEnd = kSmScratch + 256 * (8 + 4 + 8 + 4);
-constexpr uint32_t kSmWideBytes =
-    kSmRing + kRingBytes > kSmFinishEnd ? kSmRing + kRingBytes : kSmFinishEnd;
+static_assert(kSmFinishEnd <= kRingBytes, "finish scratch aliases the ring");
+// the dynamic base is below 16 KiB in practice (1 KiB driver reserve + static);
+// the kernel checks kSmMiscEnd fits under kHistAbs
+constexpr uint32_t kSmWideBytes = kHistAbs + kohler_walk::kHistBytes;
 static_assert(kSmWideBytes <= 227 * 1024, "K1 shared memory");
 
 // CTA owning unit u under the balanced partition (first cta_r CTAs hold
@@ -214,11 +224,12 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
 // Fold the packed W words (both copies) into the u64 per-CTA accumulators
 // and clear them.  Thread t owns (copy t >> 8, key t & 255): 32 lane words
 // read rotated by t & 7 so a warp's LDS.128 hit distinct bank quads.
-__device__ __forceinline__ void spill_w(unsigned char* sm, int tid)
+__device__ __forceinline__ void spill_w(unsigned char* sm, unsigned char* hist, int tid,
+                                        bool clear = true)
 {
     using namespace kohler_walk;
     const int copy = tid >> 8, key = tid & 255;
-    uint4* row = reinterpret_cast<uint4*>(sm + (key + 256 * copy) * 256 + 128);
+    uint4* row = reinterpret_cast<uint4*>(hist + (key + 256 * copy) * 256 + 128);
     uint32_t h = 0, b = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -235,7 +246,8 @@ __device__ __forceinline__ void spill_w(unsigned char* sm, int tid)
 // CTA flush of one image's partial: reduce the striped counters (clearing
 // them for the next image), form the 512 combinations, REDG them, take a
 // ticket; the last CTA of the image finishes it.
-__device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
+__device__ void flush_image(const WideParams& p, int img, unsigned char* sm, unsigned char* hist,
+                            bool clear)
 {
     using namespace kohler_walk;
     const int tid = threadIdx.x;
@@ -243,7 +255,7 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
     int* corr_tot = reinterpret_cast<int*>(sm + kSmCorrTot);
     unsigned long long* wacc = reinterpret_cast<unsigned long long*>(sm + kSmWacc);
     for (int t = tid; t < 512; t += kWalkThreads) {
-        uint4* row = reinterpret_cast<uint4*>(sm + t * 256);  // half 0: Hs[t] / dummy
+        uint4* row = reinterpret_cast<uint4*>(hist + t * 256);  // half 0: Hs[t] / dummy
         unsigned long long s = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -252,17 +264,11 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm)
             row[(j + t) & 7] = make_uint4(0, 0, 0, 0);
         }
         hs_tot[t] = s;
-        spill_w(sm, t);
+        spill_w(sm, hist, t, clear);
         if (t < 256) {
-            int4* cr = reinterpret_cast<int4*>(sm + kCorr + t * 128);
-            int cs = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int4 q = cr[(j + t) & 7];
-                cs += q.x + q.y + q.z + q.w;
-                cr[(j + t) & 7] = make_int4(0, 0, 0, 0);
-            }
-            corr_tot[t] = cs;
+            int* cr = reinterpret_cast<int*>(sm + kSmCorr);
+            corr_tot[t] = cr[t];
+            cr[t] = 0;
         }
     }
     __syncthreads();
@@ -505,8 +511,8 @@ __device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const Lan
 //   halo row (band end) : per halo pixel d under c, its owned up pair as a W
 //                         event B = 4 + sign(c - d) = 5 - q(c -> d), corr +3
 template <bool ALIGNED>
-__device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm, uint32_t smbase,
-                                         const LaneGeo& G, int r0, int r1, uint32_t lane4)
+__device__ __noinline__ void border_rows(const WideParams& p, uint32_t smbase, const LaneGeo& G,
+                                         int r0, int r1, uint32_t lane4)
 {
     using namespace kohler_walk;
     // this lane walked rows y0 + [r0, r1) of its column (clipped to its own rows)
@@ -530,7 +536,7 @@ __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm,
         uint32_t w[4];
         load16(0, w);
         for (int i = 0; i < nreal; ++i)
-            red_add(smbase + kCorr + (byte(w, i) << 7) + lane4, 1u);
+            red_add(smbase + kSmCorr + (byte(w, i) << 2), 1u);
     }
     const int ylast = G.y0 + r1 - 1;
     if (ylast == p.band_rows - 1) {
@@ -538,15 +544,15 @@ __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm,
         load16(ylast, c);
         if (p.r0 + ylast == p.h_total - 1) {
             for (int i = 0; i < nreal; ++i)
-                red_add(smbase + kCorr + (byte(c, i) << 7) + lane4, 0xFFFFFFFFu);
+                red_add(smbase + kSmCorr + (byte(c, i) << 2), 0xFFFFFFFFu);
         } else {
             uint32_t d[4];
             load16(ylast + 1, d);
             for (int i = 0; i < nreal; ++i) {
                 const uint32_t cv = byte(c, i), dv = byte(d, i);
                 const uint32_t b = 4u + (cv > dv) - (cv < dv);  // 4 + sign(c - d)
-                atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW0 + (dv << 8) + lane4), (b << 16) | 1u);
-                red_add(smbase + kCorr + (dv << 7) + lane4, 3u);
+                red_add(kHistAbs + kOffW0 + (dv << 8) + lane4, (b << 16) | 1u);
+                red_add(smbase + kSmCorr + (dv << 2), 3u);
             }
         }
     }
@@ -561,15 +567,18 @@ __device__ __noinline__ void border_rows(const WideParams& p, unsigned char* sm,
 // alternates with the position parity (bounds each copy's events).
 template <bool ALIGNED>
 __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
-                                           uint32_t smbase, const uint8_t* base, long long ua,
-                                           long long ub, bool zero_first)
+                                           unsigned char* hist, uint32_t smbase,
+                                           const uint8_t* base, long long ua, long long ub,
+                                           bool zero_first)
 {
     using namespace kohler_walk;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane4 = (uint32_t)lane * 4u;
-    const uint32_t kneg = smbase - lane4;
-    const uint32_t dummy = smbase + kDummy + lane4;
+    const uint32_t kneg = kHistAbs - lane4;  // pair event at A_a + A_b + kneg
+    const uint32_t dummy = kHistAbs + kDummy + lane4;
+    // corr[v] of a pixel with W address A: corr_base + (A >> 6) (A >> 6 = 4v + (lane4 >> 6))
+    const uint32_t corr_base = smbase + kSmCorr - (lane4 >> 6);
     const int R = p.R;
     const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
     const bool any = ua < ub;
@@ -593,9 +602,14 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     }
     if (zero_first) {
         // clear the counters while the first rows are in flight
-        uint4* z = reinterpret_cast<uint4*>(sm);
-        for (int i = threadIdx.x; i < (int)((kHistBytes + kCorrBytes + 8192) / 16); i += kWalkThreads)
+        uint4* z = reinterpret_cast<uint4*>(hist);
+        for (int i = threadIdx.x; i < (int)(kHistBytes / 16); i += kWalkThreads)
             z[i] = make_uint4(0, 0, 0, 0);
+        uint4* zw = reinterpret_cast<uint4*>(sm + kSmWacc);
+        for (int i = threadIdx.x; i < 8192 / 16; i += kWalkThreads)
+            zw[i] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x < 256)
+            reinterpret_cast<int*>(sm + kSmCorr)[threadIdx.x] = 0;
         __syncthreads();
         phase(1);
     }
@@ -665,7 +679,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 if (live) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW + C.A[i]), b_of(Be, Bo, i));
+                        red_add_imm<kHistAbs + kOffW>(C.A[i], b_of(Be, Bo, i));
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
                         red_inc(C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg);
@@ -678,17 +692,16 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const bool real = i <= G.e;
-                    atomicAdd(reinterpret_cast<uint32_t*>(sm + kOffW + C.A[i]),
-                              real ? b_of(Be, Bo, i) : 0u);
+                    red_add_imm<kHistAbs + kOffW>(C.A[i], real ? b_of(Be, Bo, i) : 0u);
                     red_inc(real ? C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg : dummy);
                     red_inc(real ? C.A[i] + D.A[i] + kneg : dummy);
                 }
             }
             if (F.edge && live) {
                 if (row_start)
-                    red_add(corr_addr(smbase, C.A[0], lane4), 1u);
+                    red_add(corr_base + (C.A[0] >> 6), 1u);
                 if (row_end)
-                    red_add(corr_addr(smbase, Arn, lane4), 0xFFFFFFFFu);
+                    red_add(corr_base + (Arn >> 6), 0xFFFFFFFFu);
             }
         };
         using K0 = std::integral_constant<int, 0>;
@@ -721,7 +734,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                                                           ((G.y0 + r0 == 0) ||
                                                            (G.y0 + min(r1, G.nrows) == p.band_rows)));
         if (border)
-            border_rows<ALIGNED>(p, sm, smbase, G, r0, r1, lane4);
+            border_rows<ALIGNED>(p, smbase, G, r0, r1, lane4);
         if (!has_next)
             break;
         pos += (uint32_t)P;
@@ -738,6 +751,9 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
 {
     extern __shared__ __align__(16) unsigned char sm[];
     const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
+    if (smbase + kSmMiscEnd > kHistAbs)
+        __trap();  // the fixed counter address would overlap the scratch (never seen)
+    unsigned char* hist = sm + (kHistAbs - smbase);
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     phase(0);
@@ -763,13 +779,13 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
                 const long long n = eb - ea;
                 const long long wa = ea + n * warp / kWalkWarps;
                 const long long wb = ea + n * (warp + 1) / kWalkWarps;
-                walk_range<ALIGNED>(p, sm, smbase, base, wa, wb, !zeroed);
+                walk_range<ALIGNED>(p, sm, hist, smbase, base, wa, wb, !zeroed);
                 warp_end();
                 zeroed = true;
                 __syncthreads();
                 if (eb < b) {
                     for (int t = tid; t < 512; t += kWalkThreads)
-                        spill_w(sm, t);
+                        spill_w(sm, hist, t);
                     __syncthreads();
                 }
             }
@@ -777,7 +793,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
                 phase(2);
                 pdl_trigger();  // the next launch may start as SMs free up
             }
-            flush_image(p, img, sm);
+            flush_image(p, img, sm, hist, img < i_last);  // the last image: no re-zeroing
             flushed = true;
         }
     }

@@ -39,7 +39,6 @@
 //   rows of 256 B, word (row, half, lane) at row*256 + half*128 + lane*4
 //   half 0, rows 0..510 : Hs[s];  row 511: dummy (neutralised events)
 //   half 1, rows 0..255 : W copy 0 (even rows);  rows 256..511: W copy 1 (odd rows)
-//   + 32 KiB corr[v][lane] at kCorr + v*128 + lane*4 (int)
 // A pixel's W address is A = (v << 8) | lane*4 (one PRMT); a pair's Hs
 // address is A_a + A_b - lane*4 = (a + b) << 8 | lane*4 (one IADD3).
 #pragma once
@@ -51,8 +50,6 @@ namespace kohler_walk {
 constexpr uint32_t kHistBytes = 512u * 256u;       // Hs / dummy / W0 / W1
 constexpr uint32_t kOffW0 = 128;
 constexpr uint32_t kOffW1 = 65536 + 128;
-constexpr uint32_t kCorr = kHistBytes;             // int[256][32]
-constexpr uint32_t kCorrBytes = 32768;
 constexpr uint32_t kDummy = 511u << 8;
 // W word = Bsum << 16 | hist.  A W lane word takes at most this many pixel
 // events between spills, so hist and Bsum <= 8 * it fit 16 bits each.
@@ -93,24 +90,15 @@ __device__ __forceinline__ void red_inc(uint32_t saddr)
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr));
 }
 
-// Pair event at shared address a + b + c (kept opaque to the front end so the
-// two adds fuse into one IADD3 instead of being re-associated around
-// common sub-expressions).
-__device__ __forceinline__ void red_inc3(uint32_t a, uint32_t b, uint32_t c)
+template <uint32_t OFF>
+__device__ __forceinline__ void red_add_imm(uint32_t saddr, uint32_t v)
 {
-    asm volatile("{\n\t.reg .u32 t;\n\tadd.u32 t, %0, %1;\n\tadd.u32 t, t, %2;\n\t"
-                 "red.shared.add.u32 [t], 1;\n\t}" ::"r"(a), "r"(b), "r"(c));
+    asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(saddr), "r"(v), "n"(OFF));
 }
 
 __device__ __forceinline__ void red_add(uint32_t saddr, uint32_t v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
-}
-
-// corr word of the pixel whose W address is A
-__device__ __forceinline__ uint32_t corr_addr(uint32_t smbase, uint32_t A, uint32_t lane4)
-{
-    return smbase + kCorr + ((A >> 8) << 7) + lane4;
 }
 
 // Unpack a loaded row into Y.  The loads already applied the border rule for
