@@ -60,6 +60,7 @@ struct WideParams {
     unsigned* tickets;  // [n]
     int k;
     int select;
+    int no_finish;  // accumulate only (a band of a chunked image; a later launch finishes)
     uint64_t* sums;
     uint64_t* cards;
     double* values;
@@ -301,6 +302,8 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
     __syncthreads();
     for (int t = tid; t < 1024; t += kWalkThreads)
         wacc[t] = 0;
+    if (p.no_finish)
+        return;  // a later launch of this image takes the tickets and finishes it
     __shared__ int s_last;
     if (tid == 0) {
         const long long first = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
@@ -1149,6 +1152,30 @@ int fail(int code, const std::string& msg)
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes)
+    {
+        if (bytes <= cap)
+            return KOHLER_OK;
+        if (p)
+            cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        KC_CUDA(cudaMallocHost(&p, bytes));
+        cap = bytes;
+        return KOHLER_OK;
+    }
+    void release()
+    {
+        if (p)
+            cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -1177,10 +1204,15 @@ struct DevBuf {
 
 } // namespace
 
+constexpr int kMaxChunks = 8;
+
 struct kohler_cuda_ctx {
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // host-API uploads, overlapped with compute
+    cudaEvent_t chunk_ev[kMaxChunks] = {};
+    cudaEvent_t done_ev = nullptr;        // compute of the previous call finished
     std::mutex mu;
     DevBuf acc;      // zero-initialised, self-cleaning
     DevBuf tickets;  // zero-initialised, self-cleaning
@@ -1188,6 +1220,7 @@ struct kohler_cuda_ctx {
     DevBuf out;      // staging for host outputs
     DevBuf curves;   // K5 curve scratch when the caller wants no curves
     DevBuf stage;    // 16-byte aligned copy of unaligned device inputs for K1
+    HostBuf hout;    // pinned staging for small results (one D2H per call)
     int last_launches = 0;
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
     bool wide_attr_set = false;
@@ -1238,7 +1271,7 @@ int check_image(int n, int w, int h, size_t pitch)
 // Launch K1 over n images whose buffers hold band_rows own rows (+ halo).
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
-                const BatchOut& o, cudaStream_t stream)
+                const BatchOut& o, cudaStream_t stream, int no_finish = 0)
 {
     if (n == 0)
         return KOHLER_OK;
@@ -1312,6 +1345,7 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
                            : 0ull;
     p.k = k;
     p.select = select;
+    p.no_finish = no_finish;
     p.sums = o.sums;
     p.cards = o.cards;
     p.values = o.values;
@@ -1489,51 +1523,141 @@ int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, si
 bool use_tile(int n, int w, int h) { return n >= 2 && (long long)w * h <= 65536; }
 
 // Stage a host batch into the device, run, copy results back.
+//
+// The upload is split into up to kMaxChunks chunks on the context's copy
+// stream, each followed (on the compute stream, after an event) by the
+// launch that consumes it, so the kernels overlap the remaining PCIe
+// transfer: a single large image is cut into row bands (each band's launch
+// accumulates into the image's shared accumulator; only the last one takes
+// the tickets and finishes the curve), a batch into contiguous image ranges.
+// Small results come back in ONE device-to-host copy.
 int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
                size_t image_stride, int k, int select, const BatchOut& host)
 {
-    const size_t dpitch = round_up((size_t)w, 128);
+    const size_t dpitch = round_up((size_t)w, 16);
     const size_t dstride = dpitch * (size_t)h;
     int rc = ctx->img.ensure(std::max<size_t>(dstride * (size_t)n, 16));
     if (rc)
         return rc;
     uint8_t* dimg = static_cast<uint8_t*>(ctx->img.p);
-    cudaStream_t st = ctx->stream;
-    if (image_stride == pitch * (size_t)h) {
-        KC_CUDA(cudaMemcpy2DAsync(dimg, dpitch, px, pitch, (size_t)w, (size_t)h * n,
-                                  cudaMemcpyHostToDevice, st));
-    } else {
-        for (int i = 0; i < n; ++i)
-            KC_CUDA(cudaMemcpy2DAsync(dimg + dstride * i, dpitch, px + image_stride * i, pitch,
-                                      (size_t)w, (size_t)h, cudaMemcpyHostToDevice, st));
-    }
-    // device outputs, packed
+    cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+    // device outputs, packed: sums | cards | values | defined | t0 | count | status | topk
     const size_t n256 = (size_t)n * 256;
-    const size_t bytes = n256 * 8 * 3 + n256 + (size_t)n * 4 * 4 + (size_t)n * k * 4 + 64;
-    rc = ctx->out.ensure(bytes);
+    const size_t tail_off = round_up(n256 * 25, 16);
+    const size_t bytes = tail_off + (size_t)n * 4 * 3 + (size_t)n * k * 4;
+    rc = ctx->out.ensure(bytes + 64);
     if (rc)
         return rc;
     char* b = static_cast<char*>(ctx->out.p);
     BatchOut d{};
-    d.sums = host.sums ? reinterpret_cast<uint64_t*>(b) : nullptr;
-    d.cards = host.cards ? reinterpret_cast<uint64_t*>(b + n256 * 8) : nullptr;
-    if (d.sums && !d.cards)
-        d.cards = reinterpret_cast<uint64_t*>(b + n256 * 8);
-    if (d.cards && !d.sums)
-        d.sums = reinterpret_cast<uint64_t*>(b);
+    const bool want_curve = true;  // curves always land in the packed block
+    d.sums = want_curve ? reinterpret_cast<uint64_t*>(b) : nullptr;
+    d.cards = want_curve ? reinterpret_cast<uint64_t*>(b + n256 * 8) : nullptr;
     d.values = host.values ? reinterpret_cast<double*>(b + n256 * 16) : nullptr;
     d.defined = host.defined ? reinterpret_cast<uint8_t*>(b + n256 * 24) : nullptr;
-    char* tail = b + n256 * 25;
-    tail = reinterpret_cast<char*>(round_up(reinterpret_cast<uintptr_t>(tail), 16));
-    d.t0s = reinterpret_cast<int*>(tail);
+    d.t0s = reinterpret_cast<int*>(b + tail_off);
     d.topk_counts = d.t0s + n;
     d.status = d.topk_counts + n;
     d.topks = d.status + n;
     ctx->last_launches = 0;
-    rc = use_tile(n, w, h) ? launch_tile(ctx, dimg, n, w, h, dpitch, dstride, k, select, d, st)
-                           : launch_wide(ctx, dimg, n, w, h, h, 0, dpitch, dstride, k, select, d, st);
-    if (rc)
-        return rc;
+
+    auto upload = [&](int i0, int i1, int y0, int y1) -> int {
+        // images [i0, i1), rows [y0, y1) of each
+        const size_t rows = (size_t)(y1 - y0);
+        if (pitch == dpitch && (i1 - i0 == 1 || image_stride == pitch * (size_t)h)) {
+            const size_t off = (size_t)i0 * dstride + (size_t)y0 * dpitch;
+            const size_t len = (i1 - i0 == 1) ? rows * dpitch : (size_t)(i1 - i0) * dstride;
+            KC_CUDA(cudaMemcpyAsync(dimg + off, px + (size_t)i0 * image_stride + (size_t)y0 * pitch,
+                                    len, cudaMemcpyHostToDevice, cs));
+        } else if (image_stride == pitch * (size_t)h && y0 == 0 && y1 == h) {
+            KC_CUDA(cudaMemcpy2DAsync(dimg + (size_t)i0 * dstride, dpitch,
+                                      px + (size_t)i0 * image_stride, pitch, (size_t)w,
+                                      (size_t)h * (i1 - i0), cudaMemcpyHostToDevice, cs));
+        } else {
+            for (int i = i0; i < i1; ++i)
+                KC_CUDA(cudaMemcpy2DAsync(dimg + dstride * i + (size_t)y0 * dpitch, dpitch,
+                                          px + image_stride * i + (size_t)y0 * pitch, pitch,
+                                          (size_t)w, rows, cudaMemcpyHostToDevice, cs));
+        }
+        return KOHLER_OK;
+    };
+    auto sub = [&](int i0) {
+        BatchOut s = d;
+        if (s.sums) {
+            s.sums += (size_t)i0 * 256;
+            s.cards += (size_t)i0 * 256;
+        }
+        if (s.values)
+            s.values += (size_t)i0 * 256;
+        if (s.defined)
+            s.defined += (size_t)i0 * 256;
+        s.t0s += i0;
+        s.topk_counts += i0;
+        s.status += i0;
+        s.topks += (size_t)i0 * k;
+        return s;
+    };
+    const bool tile = use_tile(n, w, h);
+    const size_t total = (size_t)w * h * n;
+    int chunks = (int)std::min<size_t>(kMaxChunks, std::max<size_t>(1, total / (2u << 20)));
+    if (n > 1)
+        chunks = std::min(chunks, n);
+    if (n == 1 && chunks > h)
+        chunks = h;
+    for (int c = 0; c < chunks; ++c) {
+        if (n == 1) {
+            const int a = (int)((long long)h * c / chunks), e = (int)((long long)h * (c + 1) / chunks);
+            rc = upload(0, 1, a, std::min(e + 1, h));  // + the band's halo row
+            if (rc)
+                return rc;
+            KC_CUDA(cudaEventRecord(ctx->chunk_ev[c], cs));
+            KC_CUDA(cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
+            rc = launch_wide(ctx, dimg + (size_t)a * dpitch, 1, w, e - a, h, a, dpitch, dstride, k,
+                             select, d, st, c + 1 < chunks ? 1 : 0);
+        } else {
+            const int i0 = (int)((long long)n * c / chunks), i1 = (int)((long long)n * (c + 1) / chunks);
+            rc = upload(i0, i1, 0, h);
+            if (rc)
+                return rc;
+            KC_CUDA(cudaEventRecord(ctx->chunk_ev[c], cs));
+            KC_CUDA(cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
+            const uint8_t* src = dimg + (size_t)i0 * dstride;
+            rc = tile ? launch_tile(ctx, src, i1 - i0, w, h, dpitch, dstride, k, select, sub(i0), st)
+                      : launch_wide(ctx, src, i1 - i0, w, h, h, 0, dpitch, dstride, k, select,
+                                    sub(i0), st);
+        }
+        if (rc)
+            return rc;
+    }
+    if (bytes <= (64u << 10)) {
+        // one packed copy back, then scatter on the host
+        rc = ctx->hout.ensure(bytes);
+        if (rc)
+            return rc;
+        KC_CUDA(cudaMemcpyAsync(ctx->hout.p, b, bytes, cudaMemcpyDeviceToHost, st));
+        KC_CUDA(cudaStreamSynchronize(st));
+        const char* hb = static_cast<const char*>(ctx->hout.p);
+        if (host.sums)
+            std::memcpy(host.sums, hb, n256 * 8);
+        if (host.cards)
+            std::memcpy(host.cards, hb + n256 * 8, n256 * 8);
+        if (host.values)
+            std::memcpy(host.values, hb + n256 * 16, n256 * 8);
+        if (host.defined)
+            std::memcpy(host.defined, hb + n256 * 24, n256);
+        if (select) {
+            const int* ht = reinterpret_cast<const int*>(hb + tail_off);
+            if (host.t0s)
+                std::memcpy(host.t0s, ht, (size_t)n * 4);
+            if (host.topk_counts)
+                std::memcpy(host.topk_counts, ht + n, (size_t)n * 4);
+            if (host.status)
+                std::memcpy(host.status, ht + 2 * n, (size_t)n * 4);
+            if (host.topks)
+                std::memcpy(host.topks, ht + 3 * n, (size_t)n * k * 4);
+        }
+        return KOHLER_OK;
+    }
     if (host.sums)
         KC_CUDA(cudaMemcpyAsync(host.sums, d.sums, n256 * 8, cudaMemcpyDeviceToHost, st));
     if (host.cards)
@@ -1589,6 +1713,12 @@ int kohler_cuda_create(int device, kohler_cuda_ctx** out)
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < kMaxChunks && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&ctx->chunk_ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&ctx->done_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete ctx;
         return fail(KOHLER_CUDA_ERROR, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
@@ -1610,7 +1740,15 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         ctx->out.release();
         ctx->curves.release();
         ctx->stage.release();
+        ctx->hout.release();
         cudaStreamDestroy(ctx->stream);
+        if (ctx->copy_stream)
+            cudaStreamDestroy(ctx->copy_stream);
+        for (int i = 0; i < kMaxChunks; ++i)
+            if (ctx->chunk_ev[i])
+                cudaEventDestroy(ctx->chunk_ev[i]);
+        if (ctx->done_ev)
+            cudaEventDestroy(ctx->done_ev);
     }
     delete ctx;
 }
