@@ -155,18 +155,38 @@ __device__ __forceinline__ void phase(int) {}
 __device__ __forceinline__ void warp_end() {}
 #endif
 
-// Last CTA of an image: sum accumulator copies, reset them, rebuild the
-// curve (K3: int64 prefix scans), write it, and (optionally) select (K4).
-__device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
-{
-    const int tid = threadIdx.x;
-    long long* sval = reinterpret_cast<long long*>(sm + kSmVal);
-    uint64_t* csum = reinterpret_cast<uint64_t*>(sm + kSmCurve);
-    uint64_t* ccard = csum + 256;
-    double* mean = reinterpret_cast<double*>(sm + kSmMean);
-    uint8_t* def = sm + kSmDef;
+// K3 + K4, one CTA (256 threads) per image, launched right after K1 with
+// programmatic dependent launch: waits for K1, sums the accumulator copies
+// (resetting them: the workspace is self-cleaning), rebuilds count/sum with
+// int64 prefix scans, writes the curve and the IEEE f64 mean curve, selects.
+struct FinishParams {
+    unsigned long long* acc;  // [n][copies][512]
+    int copies;
+    int k;
+    int select;
+    uint64_t* sums;
+    uint64_t* cards;
+    double* values;
+    uint8_t* defined;
+    int* t0s;
+    int* topks;
+    int* topk_counts;
+    int* status;
+};
 
-    for (int r = tid; r < 512; r += kWalkThreads) {
+__global__ void __launch_bounds__(256) finish_kernel(const FinishParams p)
+{
+    __shared__ long long sval[512];
+    __shared__ long long tmp[256];
+    __shared__ uint64_t csum[256], ccard[256];
+    __shared__ double mean[256];
+    __shared__ uint8_t def[256];
+    __shared__ __align__(16) unsigned char scr[256 * (8 + 4 + 8 + 4) + 64];
+    const int tid = threadIdx.x;
+    const int img = blockIdx.x;
+    pdl_trigger();  // the next K1 may start its walk; its flush waits for us
+    pdl_wait();     // K1's accumulation of this image is complete and visible
+    for (int r = tid; r < 512; r += 256) {
         unsigned long long* a = p.acc + (size_t)img * p.copies * 512 + r;
         unsigned long long v[kAccCopiesSingle];
 #pragma unroll
@@ -181,12 +201,8 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
         }
         sval[r] = (long long)s;
     }
-    if (tid == 0)
-        p.tickets[img] = 0;
     __syncthreads();
-    phase(4);
     const int warp = tid >> 5;
-    long long* tmp = reinterpret_cast<long long*>(sm + kSmHsTot);  // free here
     if (warp == 0)
         warp_prefix256(sval, reinterpret_cast<long long*>(ccard));
     else if (warp == 1) {
@@ -195,7 +211,7 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
         warp_prefix256(tmp, reinterpret_cast<long long*>(csum));
     }
     __syncthreads();
-    if (tid < 256) {
+    {
         const uint64_t cs = csum[tid], cc = ccard[tid];
         const double v = cc ? (double)cs / (double)cc : 0.0;
         mean[tid] = v;
@@ -210,16 +226,13 @@ __device__ void finish_image(const WideParams& p, int img, unsigned char* sm)
             p.defined[(size_t)img * 256 + tid] = cc ? 1 : 0;
     }
     __syncthreads();
-    phase(5);
-    if (p.select && tid < 256) {
-        const int st = block_select256(mean, def, p.k, sm + kSmScratch, 1,
-                                       p.t0s ? p.t0s + img : nullptr,
+    if (p.select) {
+        const int st = block_select256(mean, def, p.k, scr, 1, p.t0s ? p.t0s + img : nullptr,
                                        p.topks ? p.topks + (size_t)img * p.k : nullptr,
                                        p.topk_counts ? p.topk_counts + img : nullptr);
         if (tid == 0 && p.status)
             p.status[img] = st;
     }
-    phase(6);
 }
 
 // Fold the packed W words (both copies) into the u64 per-CTA accumulators
@@ -245,8 +258,8 @@ __device__ __forceinline__ void spill_w(unsigned char* sm, unsigned char* hist, 
 }
 
 // CTA flush of one image's partial: reduce the striped counters (clearing
-// them for the next image), form the 512 combinations, REDG them, take a
-// ticket; the last CTA of the image finishes it.
+// them for the next image), form the 512 combinations, REDG them into the
+// image's accumulator (finish_kernel takes it from there).
 __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, unsigned char* hist,
                             bool clear)
 {
@@ -273,8 +286,7 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
         }
     }
     __syncthreads();
-    // the workspace (acc, tickets) and outputs may still be in use by the
-    // previous launch in this stream
+    // the accumulators may still be read / reset by the previous finish_kernel
     pdl_wait();
     for (int t = tid; t < 512; t += kWalkThreads) {
         auto hist = [&](int v) { return (long long)(wacc[v] + wacc[512 + v]); };
@@ -298,27 +310,10 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
             atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + t, (unsigned long long)val);
         }
     }
-    __threadfence();
     __syncthreads();
     for (int t = tid; t < 1024; t += kWalkThreads)
         wacc[t] = 0;
-    if (p.no_finish)
-        return;  // a later launch of this image takes the tickets and finishes it
-    __shared__ int s_last;
-    if (tid == 0) {
-        const long long first = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
-        const long long last = cta_of_unit((long long)(img + 1) * p.upi - 1, p.cta_q, p.cta_r);
-        const unsigned expected = (unsigned)(last - first + 1);
-        const unsigned prev = atomicAdd(p.tickets + img, 1u);
-        s_last = (prev + 1 == expected);
-    }
-    __syncthreads();
     phase(3);
-    if (s_last) {
-        __threadfence();
-        finish_image(p, img, sm);
-    }
-    __syncthreads();
 }
 
 // A lane's 16-pixel segment: unit u covers flattened (row, segment) indices
@@ -1268,6 +1263,23 @@ int check_image(int n, int w, int h, size_t pitch)
     return KOHLER_OK;
 }
 
+template <class Kern, class Arg>
+cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                       const Arg& arg)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, arg);
+}
+
 // Launch K1 over n images whose buffers hold band_rows own rows (+ halo).
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
@@ -1401,27 +1413,28 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<true>, p));
     else
         KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<false>, p));
-    KC_CUDA(cudaGetLastError());
     ctx->last_launches += 1;
+    if (!no_finish) {
+        FinishParams fp{};
+        fp.acc = p.acc;
+        fp.copies = copies;
+        fp.k = k;
+        fp.select = select;
+        fp.sums = o.sums;
+        fp.cards = o.cards;
+        fp.values = o.values;
+        fp.defined = o.defined;
+        fp.t0s = o.t0s;
+        fp.topks = o.topks;
+        fp.topk_counts = o.topk_counts;
+        fp.status = o.status;
+        KC_CUDA(launch_pdl(finish_kernel, (unsigned)n, 256, 0, stream, fp));
+        ctx->last_launches += 1;
+    }
+    KC_CUDA(cudaGetLastError());
     return KOHLER_OK;
 }
 
-template <class Kern, class Arg>
-cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
-                       const Arg& arg)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, arg);
-}
 
 int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t stream)
 {

@@ -191,3 +191,265 @@ __device__ __forceinline__ uint32_t b_of(const uint32_t (&Be)[4], const uint32_t
 }
 
 } // namespace kohler_walk
+
+// ---- single-warp finish for 256-level curves (K3 + K4) --------------------
+//
+// One warp, lane L owning thresholds t = 8L .. 8L+7 in registers, restates
+// proj/src/threshold.cpp exactly (for finite values):
+//   mean_contrast (:9-23)       values[t] = (double)sum / (double)card, defined iff card > 0
+//   optimal_threshold (:25-37)  argmax over defined t, ties to the smallest t
+//   top_k_local_maxima (:39-82) collapse equal-valued runs of the defined
+//                               subsequence (first t kept), keep runs strictly
+//                               above both neighbouring runs (one-sided at the
+//                               ends), rank by (value desc, t asc), keep k,
+//                               report ascending.
+// Cross-lane information moves by warp scans of per-lane summaries:
+//   prefix: the last defined value left of a lane;
+//   suffix: the value of the leftmost run right of a lane and the value of
+//           the run after it (a run may continue across lanes).
+namespace kohler_walk {
+
+struct RunSum {      // summary of a range of thresholds (its defined entries)
+    int has;         // any defined entry
+    double lv;       // leftmost run value
+    int lnext_has;   // a second run exists
+    double lnext;    // value of the run after the leftmost run
+};
+
+__device__ __forceinline__ RunSum runsum_combine(const RunSum& A, const RunSum& B)
+{
+    // A left of B
+    if (!A.has)
+        return B;
+    if (!B.has)
+        return A;
+    RunSum r;
+    r.has = 1;
+    r.lv = A.lv;
+    if (A.lnext_has) {
+        r.lnext_has = 1;
+        r.lnext = A.lnext;
+    } else if (A.lv == B.lv) {  // A is one run continuing into B's leftmost run
+        r.lnext_has = B.lnext_has;
+        r.lnext = B.lnext;
+    } else {
+        r.lnext_has = 1;
+        r.lnext = B.lv;
+    }
+    return r;
+}
+
+__device__ __forceinline__ RunSum runsum_shfl_down(const RunSum& x, int off)
+{
+    RunSum y;
+    y.has = __shfl_down_sync(0xFFFFFFFFu, x.has, off);
+    y.lv = __shfl_down_sync(0xFFFFFFFFu, x.lv, off);
+    y.lnext_has = __shfl_down_sync(0xFFFFFFFFu, x.lnext_has, off);
+    y.lnext = __shfl_down_sync(0xFFFFFFFFu, x.lnext, off);
+    return y;
+}
+
+// better (value desc, t asc) of two candidates; t < 0 = none
+__device__ __forceinline__ void best_of(double& bv, int& bt, double ov, int ot)
+{
+    if (ot >= 0 && (bt < 0 || ov > bv || (ov == bv && ot < bt))) {
+        bv = ov;
+        bt = ot;
+    }
+}
+
+// v/d: this lane's 8 values / defined flags (t = 8 lane + j).  mv/mt: smem
+// scratch for the maxima (>= 128 entries).  Returns 1 (no boundary) or 0.
+__device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int k, double* mv,
+                                   int* mt, int* out_t0, int* out_topk, int* out_count)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // optimal threshold
+    double bv = 0.0;
+    int bt = -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (d[j] && (bt < 0 || v[j] > bv)) {
+            bv = v[j];
+            bt = 8 * lane + j;
+        }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, off);
+        const int ot = __shfl_xor_sync(0xFFFFFFFFu, bt, off);
+        best_of(bv, bt, ov, ot);
+    }
+    if (bt < 0) {  // nothing defined: NoBoundaryError
+        if (lane == 0) {
+            if (out_t0)
+                *out_t0 = -1;
+            if (out_count)
+                *out_count = 0;
+        }
+        return 1;
+    }
+    // prefix: last defined value strictly left of this lane
+    int ph = 0;
+    double pv = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (d[j]) {
+            ph = 1;
+            pv = v[j];
+        }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int oh = __shfl_up_sync(0xFFFFFFFFu, ph, off);
+        const double ov = __shfl_up_sync(0xFFFFFFFFu, pv, off);
+        if (lane >= off && !ph) {
+            ph = oh;
+            pv = ov;
+        }
+    }
+    int cin_h = __shfl_up_sync(0xFFFFFFFFu, ph, 1);
+    double cin_v = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+    if (lane == 0)
+        cin_h = 0;
+    // suffix: run summary of everything right of this lane
+    RunSum mine{0, 0.0, 0, 0.0};
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+        if (d[j]) {
+            RunSum e{1, v[j], 0, 0.0};
+            mine = runsum_combine(e, mine);
+        }
+    }
+    RunSum suf = mine;  // inclusive suffix over lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const RunSum o = runsum_shfl_down(suf, off);
+        if (lane + off < 32)
+            suf = runsum_combine(suf, o);
+    }
+    RunSum right = runsum_shfl_down(suf, 1);  // lanes > lane
+    if (lane == 31)
+        right.has = 0;
+    // per entry, right to left: value of the next run after the entry's run
+    // (nr_has/nr), tracking the run the entry belongs to (cur)
+    bool is_start[8];
+    double nxt[8];
+    bool nxt_has[8];
+    {
+        int ch = right.has;
+        double cv = right.lv;                 // value of the run right of here
+        int nh = right.lnext_has;
+        double nv = right.lnext;              // and the run after it
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            if (d[j]) {
+                if (!ch) {
+                    ch = 1;
+                    cv = v[j];
+                    nh = 0;
+                } else if (v[j] != cv) {
+                    nh = 1;
+                    nv = cv;
+                    cv = v[j];
+                }
+                nxt_has[j] = nh;
+                nxt[j] = nv;
+            } else {
+                nxt_has[j] = false;
+                nxt[j] = 0.0;
+            }
+        }
+    }
+    // left to right: run starts and their maxima
+    unsigned maxmask = 0;
+    {
+        int hh = cin_h;
+        double hv = cin_v;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            is_start[j] = false;
+            if (d[j]) {
+                is_start[j] = !hh || v[j] != hv;
+                if (is_start[j] && (!hh || hv < v[j]) && (!nxt_has[j] || nxt[j] < v[j]))
+                    maxmask |= 1u << j;
+                hh = 1;
+                hv = v[j];
+            }
+        }
+    }
+    // compact the maxima in t order
+    const int myn = __popc(maxmask);
+    int pre = myn;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xFFFFFFFFu, pre, off);
+        if (lane >= off)
+            pre += o;
+    }
+    const int nm = __shfl_sync(0xFFFFFFFFu, pre, 31);
+    int pos = pre - myn;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (maxmask & (1u << j)) {
+            mv[pos] = v[j];
+            mt[pos] = 8 * lane + j;
+            ++pos;
+        }
+    __syncwarp();
+    // top-k: k rounds of warp argmax over the maxima (<= 128: 4 per lane)
+    double cv[4];
+    int ct[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        ct[q] = i < nm ? mt[i] : -1;
+        cv[q] = i < nm ? mv[i] : 0.0;
+    }
+    unsigned sel = 0;  // bit q: candidate lane + 32 q selected
+    if (k >= nm) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (ct[q] >= 0)
+                sel |= 1u << q;
+    } else {
+        for (int r = 0; r < k; ++r) {
+            double lv = 0.0;
+            int ltt = -1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (!(sel & (1u << q)))
+                    best_of(lv, ltt, cv[q], ct[q]);
+            double gv = lv;
+            int gt = ltt;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xFFFFFFFFu, gv, off);
+                const int ot = __shfl_xor_sync(0xFFFFFFFFu, gt, off);
+                best_of(gv, gt, ov, ot);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (ct[q] == gt)
+                    sel |= 1u << q;
+        }
+    }
+    // report ascending t: candidates are in t order (index lane + 32 q)
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const bool s = (sel >> q) & 1u;
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, s);
+        if (s && out_topk)
+            out_topk[cnt + __popc(b & lt)] = ct[q];
+        cnt += __popc(b);
+    }
+    if (lane == 0) {
+        if (out_t0)
+            *out_t0 = bt;
+        if (out_count)
+            *out_count = cnt;
+    }
+    return 0;
+}
+
+} // namespace kohler_walk
