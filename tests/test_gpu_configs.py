@@ -113,3 +113,38 @@ def test_c5_small_images_vs_reference(ctx, ref):
     assert np.all(r["status"][fam_b] == 1) and np.all(r["t0"][fam_b] == -1)
     assert not r["cards"][fam_b].any()
     assert np.all(r["status"][~fam_b] == 0)
+
+
+def host_result(r):
+    return {"sums": r.sums, "cards": r.cards, "values": r.values, "t0": r.t0,
+            "topk": r.topk, "topk_count": r.topk_count, "status": r.status}
+
+
+def test_host_api_chunked_single_image_vs_reference(ctx, ref):
+    """Host API on C2: the upload is cut into row bands whose launches
+    accumulate into one image (only the last finishes) — bit-exact."""
+    x = synth.generate("C2", device="cpu").numpy()
+    r = host_result(ctx.analyze_batch(x, K))
+    exp = ref.analyze_batch(x, K, workers=8, threads=1)
+    check_against_reference(r, exp)
+
+
+@pytest.mark.parametrize("hw", [(2001, 1771), (1, 5_000_000), (4_200_000, 1)])
+def test_host_api_chunked_ragged_and_degenerate(ctx, ref, hw):
+    """Ragged width, a 1-pixel-wide column and a 1-row image through the
+    chunked host path (bands of one row, halo rows at every chunk edge)."""
+    h, w = hw
+    rng = np.random.default_rng(h * 7 + w)
+    x = rng.integers(0, 256, size=(1, h, w), dtype=np.uint8)
+    x[0, : h // 2] //= 3  # two regimes
+    r = host_result(ctx.analyze_batch(x, K))
+    exp = ref.analyze_batch(x, K, workers=8, threads=1)
+    check_against_reference(r, exp)
+
+
+def test_host_api_chunked_batch_vs_reference(ctx, ref):
+    """Host API on 24 C3 frames: image-range chunks, each its own launch."""
+    x = synth.generate("C3", device="cpu")[:24].numpy()
+    r = host_result(ctx.analyze_batch(x, K))
+    exp = ref.analyze_batch(x, K, workers=1)
+    check_against_reference(r, exp)
