@@ -89,9 +89,11 @@ constexpr uint32_t kHistAbs = 0x10000;
 // slots of 32 lane segments + a 16-byte pad on each side.  Idle during the
 // flush, so the reconstruction / selection scratch aliases it.
 constexpr int kRingSlots = 4;
-constexpr uint32_t kSlotBytes = 16 + 32 * 16 + 16;
-constexpr uint32_t kSmRing = 0;
-constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlotBytes;
+// slot: 32 lane segments (512 B, 128-byte aligned: cp.async writes whole
+// lines), then the left pad (lane 0) and the right pad (lane 31)
+constexpr uint32_t kSlotBytes = 640;
+constexpr uint32_t kSmRing = 0;  // + up to 127 B to align the ring to 128 B
+constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlotBytes + 128;
 constexpr uint32_t kSmWacc = kSmRing + kRingBytes;   // u64 [2 copies][2 fields][256]
 constexpr uint32_t kSmHsTot = kSmWacc + 8192;        // u64[512]
 constexpr uint32_t kSmCorrTot = kSmHsTot + 4096;     // int[256]
@@ -417,7 +419,8 @@ __device__ __forceinline__ void process(const Geo& p, unsigned char* sm, int y, 
 struct LaneGeo {
     const uint8_t* p;  // row y0 - 1, column x0 (dereferenced only for valid rows)
     uint32_t pad;      // lane 0 / 31: also copy the 16 bytes left / right (neighbour exists)
-    int pd;            // -16 (lane 0) or +16
+    int pd;            // -16 (lane 0) or +16: global offset of the pad copy
+    int pds;           // shared offset of the pad copy from the lane's segment
     int x0;
     int y0;            // first own row (band-relative)
     int nrows;         // own rows of the walk (0: no task)
@@ -450,6 +453,7 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
     }
     L.p = base + ((long long)L.y0 - 1) * (long long)p.pitch + L.x0;
     L.pd = lane == 0 ? -16 : 16;
+    L.pds = lane == 0 ? 512 : 528 - 16 * 31;
     L.pad = ((lane == 0) & (L.x0 > 0)) | ((lane == 31) & (L.e > 15)) ? 1u : 0u;
     return L;
 }
@@ -467,7 +471,7 @@ __device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitc
         "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
         "@p cp.async.cg.shared.global [%3], [%4], 16;\n\t"
         "cp.async.commit_group;\n\t}" ::"r"(dst),
-        "l"(src), "r"(L.pad), "r"(dst + L.pd), "l"(src + L.pd)
+        "l"(src), "r"(L.pad), "r"(dst + L.pds), "l"(src + L.pd)
         : "memory");
 }
 
@@ -492,7 +496,7 @@ struct GroupFlags {
     bool ragged;  // some lane's segment runs past the row end (garbage bytes)
 };
 
-__device__ __forceinline__ GroupFlags group_flags(const WideParams& p, const LaneGeo& L, bool aligned)
+__device__ __forceinline__ GroupFlags group_flags(const LaneGeo& L, bool aligned)
 {
     GroupFlags f;
     const bool act = L.nrows > 0;
@@ -581,8 +585,8 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
     const bool any = ua < ub;
     // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
-    const uint32_t seg0 = smbase + kSmRing + (uint32_t)warp * (kRingSlots * kSlotBytes) + 16u +
-                          (uint32_t)lane * 16u;
+    const uint32_t ring = (smbase + kSmRing + 127u) & ~127u;
+    const uint32_t seg0 = ring + (uint32_t)warp * (kRingSlots * kSlotBytes) + (uint32_t)lane * 16u;
 
     // current segment: group g, rows [r0, r1) of its walks; next segment
     long long g = 0;
@@ -623,10 +627,12 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         const bool has_next = gn * R < ub;
         const int nr1 = has_next ? (int)(ub - gn * R < (long long)R ? (int)(ub - gn * R) : R) : 0;
         const LaneGeo N = has_next ? lane_geo(p, base, gn, lane) : G;
-        const GroupFlags F = group_flags(p, G, ALIGNED);
+        const GroupFlags F = group_flags(G, ALIGNED);
         const bool row_start = G.x0 == 0, row_end = G.e <= 15;
-        const uint32_t offl = G.x0 > 0 ? 0xFFFFFFFFu : 0u;  // left neighbour byte
-        const uint32_t offr = G.e > 15 ? 16u : 15u;         // right neighbour byte
+        // neighbour bytes: the adjacent lane's segment, lanes 0 / 31 their pad,
+        // a row start / end the pixel itself
+        const uint32_t offl = G.x0 == 0 ? 0u : lane == 0 ? 512u + 15u : 0xFFFFFFFFu;
+        const uint32_t offr = G.e <= 15 ? 15u : lane == 31 ? 528u - 16u * 31u : 16u;
 
         // One ring position j: prefetch position j + 3 (of this segment or,
         // past its end, of the next), absorb row r0 - 1 + j into D and
@@ -801,218 +807,341 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
 }
 
 // ---------------------------------------------------------------------------
-// K5 tile_kernel: batches of small images.  The 32 lane copies of the striped
-// histogram are split into NG = 32/LG groups of LG lanes; group g of every
-// warp accumulates image i0+g, so one CTA accumulates NG whole images at once
-// and pays ONE histogram flush per NG images.  Each image is owned by a
-// single CTA, so its curve is rebuilt in the CTA (no global accumulators, no
-// tickets) and written straight to the outputs; selection runs in a
-// throughput pass (select_kernel, one warp per curve) right after.
+// K5 twalk_kernel: batches of small images with the three-event column walk.
+// The 32 lanes of every warp are split into NG = 32/LG lane groups; group g
+// of all 16 warps walks image i0 + g of the round, so the image's counters
+// are exactly its LG lane stripes of the shared block (conflict free across
+// images) and one round accumulates NG whole images.  Walker (warp w, lane
+// l in group g) takes task w*LG + l of its image: segment column task % S,
+// rows [R*(task/S), +R).  Each group's first / last lane also copies the 16
+// bytes left / right of the group's run into the group's pads.  After the
+// walk, warp g rebuilds image i0+g's curve straight from its stripes (K3) and
+// zeroes them; the per-image selection runs in select_kernel (K4).
 // ---------------------------------------------------------------------------
-struct TileParams {
+struct TwParams {
     const uint8_t* px;
     size_t pitch;
     size_t image_stride;
-    int n;
-    int w;
-    int h;
-    int nseg;
-    int segs;  // h * nseg
+    int n, w, h;
+    int S;  // segments per row
+    int R;  // rows per walk
+    int C;  // walk chunks per image (S * C <= 16 * LG)
     uint64_t* sums;
     uint64_t* cards;
 };
 
-constexpr uint32_t kTileCorr = kStripedBytes;  // int[256][32] lane-striped
-// Per image group, the reduced histograms in a padded layout that makes the
-// lane-blocked reads of warp_curve256 bank-conflict free: hist/hhi/corr at
-// pad8(x) = x + (x >> 5) (264 words each), hs at pad16(s) = s + (s >> 4) (544).
-constexpr int kTileGroupWords = 264 * 3 + 544;                       // 1336
-constexpr uint32_t kTileTot = kTileCorr + 32768;                     // u32[NG][1336]
-constexpr uint32_t kTileBytes = kTileTot + 8 * kTileGroupWords * 4;  // ~203 KiB
+// K5 per-image totals scratch (u32, padded): hs[512] at pad16, then
+// h0, b0, h1, b1 [256] at pad8 (kTwArr words each)
+constexpr int kTwArr = 288;                               // pad8(255) = 286
+constexpr int kTwH = 560;                                 // pad16(511) = 542
+__device__ __forceinline__ int pad8(int x) { return x + (x >> 3); }    // 9*lane + j: conflict free
+__device__ __forceinline__ int pad16(int x) { return x + (x >> 4); }   // 17*lane + c
+constexpr int kTwImgWords = (kTwH + 4 * kTwArr + 3) / 4 * 4;
 
-__device__ __forceinline__ int pad8(int x) { return x + (x >> 5); }
-__device__ __forceinline__ int pad16(int x) { return x + (x >> 4); }
+template <int LG>
+struct TwLayout {
+    static constexpr int NG = 32 / LG;
+    // 32 lane segments (512 B, 128-byte aligned), then 2 pads per group
+    static constexpr uint32_t kSlot = (512 + 32 * NG + 127) / 128 * 128;
+    static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
+    static constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlot + 128;
+    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][256]
+    static constexpr uint32_t kEnd = kCorr + NG * 1024;
+    static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
+};
 
-template <bool VEC, bool ALIGNED, int LG>
-__global__ void __launch_bounds__(kWideThreads, 1) tile_kernel(const TileParams p)
+__device__ __forceinline__ LaneGeo tw_geo(const TwParams& p, long long img, int task)
 {
-    constexpr int NG = 32 / LG;
-    constexpr int TG = 32 * LG;  // threads per image group
-    extern __shared__ __align__(16) unsigned char sm[];
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int g = lane / LG;
-    const int tg = warp * LG + (lane % LG);
-    const uint32_t lane4 = (uint32_t)lane * 4u;
-    uint32_t* tot = reinterpret_cast<uint32_t*>(sm + kTileTot);
-    const Geo geo{p.pitch, p.w, p.h, 0, p.h};
-    const StripedCorr pcorr{sm + kTileCorr, lane4};
-    const int rounds_steps = (p.segs + TG - 1) / TG;  // warp-uniform trip count
-    const int aq = TG / p.nseg, ar = TG % p.nseg;
+    LaneGeo L;
+    const bool act = img < p.n && task < p.S * p.C;
+    const int s = act ? task % p.S : 0;
+    const int c = act ? task / p.S : 0;
+    L.x0 = s << 4;
+    L.e = p.w - 1 - L.x0;
+    if (act) {
+        L.y0 = c * p.R;
+        L.nrows = min(p.R, p.h - L.y0);
+        L.jlo = L.y0 == 0 ? 1 : 0;
+        L.jcl = p.h - L.y0;
+    } else {
+        L.y0 = 1;
+        L.nrows = 0;
+        L.jlo = 0;
+        L.jcl = 0;
+    }
+    L.p = p.px + (size_t)(act ? img : 0) * p.image_stride + (long long)(L.y0 - 1) * (long long)p.pitch +
+          L.x0;
+    return L;
+}
 
+template <bool ALIGNED, int LG>
+__global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p)
+{
+    using namespace kohler_walk;
+    using Lay = TwLayout<LG>;
+    constexpr int NG = Lay::NG;
+    extern __shared__ __align__(16) unsigned char sm[];
+    const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
+    if (smbase + Lay::kEnd > kHistAbs)
+        __trap();
+    unsigned char* hist = sm + (kHistAbs - smbase);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane / LG, lig = lane % LG;
+    const uint32_t lane4 = (uint32_t)lane * 4u;
+    const uint32_t kneg = kHistAbs - lane4;
+    const uint32_t dummy = kHistAbs + kDummy + lane4;
+    const uint32_t corr_g = smbase + Lay::kCorr + (uint32_t)g * 1024u;
+    const uint32_t corr_base = corr_g - (lane4 >> 6);
+    const uint32_t pitch = (uint32_t)p.pitch;
+    const int task = warp * LG + lig;
+    const int P = p.R + 2;
+    const uint32_t ring = (smbase + Lay::kRing + 127u) & ~127u;
+    const uint32_t seg0 = ring + (uint32_t)warp * (kRingSlots * Lay::kSlot) + (uint32_t)lane * 16u;
+    const uint32_t padl = 512u + 32u * g - 16u * lane;  // group pads, relative to the segment
+    const uint32_t padr = padl + 16u;
+    auto geo = [&](long long i0) {
+        LaneGeo L = tw_geo(p, i0 + g, task);
+        L.pd = lig == 0 ? -16 : 16;
+        L.pds = (int)(lig == 0 ? padl : padr);
+        L.pad = ((lig == 0) & (L.x0 > 0)) | ((lig == LG - 1) & (L.e > 15)) ? 1u : 0u;
+        return L;
+    };
+    const long long stride = (long long)gridDim.x * NG;
+    long long i0 = (long long)blockIdx.x * NG;
+    LaneGeo G = geo(i0);
+    fetch_row(G, 0, pitch, seg0);
+    fetch_row(G, 1, pitch, seg0 + Lay::kSlot);
+    fetch_row(G, 2, pitch, seg0 + 2 * Lay::kSlot);
     {
-        uint4* z = reinterpret_cast<uint4*>(sm);
-        for (int i = tid; i < (int)((kStripedBytes + 32768) / 16); i += kWideThreads)
+        uint4* z = reinterpret_cast<uint4*>(hist);
+        for (int i = tid; i < (int)(kHistBytes / 16); i += kWalkThreads)
             z[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < NG * 256; i += kWalkThreads)
+            reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
     }
     __syncthreads();
     bool waited = false;
-#ifdef KOHLER_PHASES
-    unsigned long long t_acc = 0, t_red = 0, t_mark = clock64();
-#endif
-
-    // first segment of this thread in image `im` (or an inactive position)
-    auto start_pos = [&](long long im, Cursor& c) {
-        c.y = tg / p.nseg;
-        c.seg = tg - c.y * p.nseg;
-        if (im >= p.n)
-            c.y = p.h;  // inactive lane: no loads, no updates
-    };
-    auto image_base = [&](long long im) {
-        return p.px + (size_t)(im < p.n ? im : 0) * p.image_stride;
-    };
-    const long long stride_i0 = (long long)gridDim.x * NG;
-    Segment A, B;
-    A.rn = B.rn = 0;
-    {
-        Cursor cs0;
-        const long long im0 = (long long)blockIdx.x * NG + g;
-        start_pos(im0, cs0);
-        fetch<VEC>(geo, image_base(im0), cs0.y, cs0.seg, A);
-    }
-
-    for (long long i0 = (long long)blockIdx.x * NG; i0 < p.n; i0 += stride_i0) {
-        const long long img = i0 + g;
-        const uint8_t* base = image_base(img);
-        const long long img_next = img + stride_i0;
-        Cursor c0, c1, cn;
-        start_pos(img, c0);
-        start_pos(img_next, cn);
-        c1 = c0;
-        c1.advance(p.nseg, aq, ar);
-        int rem = rounds_steps;
-        bool next_in_b = false;
-        // A holds the round's first segment (prefetched during the previous
-        // round); the last step prefetches the next round's first segment
-        while (rem > 0) {
-            if (rem > 1)
-                fetch<VEC>(geo, base, c1.y, c1.seg, B);
-            else {
-                fetch<VEC>(geo, image_base(img_next), cn.y, cn.seg, B);
-                next_in_b = true;
-            }
-            process<ALIGNED>(geo, sm, c0.y, c0.seg, lane4, A, pcorr);
-            if (--rem == 0)
-                break;
-            c0 = c1;
-            c0.advance(p.nseg, aq, ar);
-            if (rem > 1)
-                fetch<VEC>(geo, base, c0.y, c0.seg, A);
-            else {
-                fetch<VEC>(geo, image_base(img_next), cn.y, cn.seg, A);
-                next_in_b = false;
-            }
-            process<ALIGNED>(geo, sm, c1.y, c1.seg, lane4, B, pcorr);
-            --rem;
-            c1 = c0;
-            c1.advance(p.nseg, aq, ar);
-        }
-        if (next_in_b)
-            A = B;
-        __syncthreads();
-#ifdef KOHLER_PHASES
-        { const unsigned long long t = clock64(); t_acc += t - t_mark; t_mark = t; }
-#endif
-        {
-            // reduce: thread t owns (row t>>1, half t&1); image group gr's
-            // lanes are the NQ consecutive uint4 [gr*NQ, gr*NQ+NQ) of the row,
-            // visited in an order rotated by t so a warp hits distinct banks
-            constexpr int NQ = LG / 4;
-            const int r = tid >> 1, hf = tid & 1;
-            uint4* row = reinterpret_cast<uint4*>(sm + r * 256 + hf * 128);
-            const int dst = hf ? (r < 256 ? pad8(r) : 264 + pad8(r - 256)) : 2 * 264 + pad16(r);
+    Car X, Y;
+    uint32_t pos = 0;
+    for (; i0 < p.n; i0 += stride) {
+        const bool has_next = i0 + stride < p.n;
+        LaneGeo N = G;
+        const GroupFlags F = group_flags(G, ALIGNED);
+        const bool row_start = G.x0 == 0, row_end = G.e <= 15;
+        const uint32_t offl = G.x0 == 0 ? 0u : lig == 0 ? padl + 15u : 0xFFFFFFFFu;
+        const uint32_t offr = G.e <= 15 ? 15u : lig == LG - 1 ? padr : 16u;
+        auto step = [&](Car& D, Car& C, int j, auto kind, auto wc, auto cross) {
+            constexpr int KIND = decltype(kind)::value;
+            constexpr int WC = decltype(wc)::value;
+            constexpr bool CROSS = decltype(cross)::value;
+            constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
+            const uint32_t q = pos + (uint32_t)j;
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncwarp();
+            const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
+            if (!CROSS || j + 3 < P)
+                fetch_row(G, j + 3, pitch, pref);
+            else if (has_next)
+                fetch_row(N, j + 3 - P, pitch, pref);
+            else
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            Row r;
+            read_row(r, seg0 + (q & 3u) * Lay::kSlot, offl, offr);
+            absorb<ALIGNED>(D, r, lane4, G.e);
+            if (KIND == 1) {
+                const bool has_up = G.y0 > 0;
 #pragma unroll
-            for (int kk = 0; kk < NG; ++kk) {
-                const int gr = (kk + tid) & (NG - 1);
-                uint32_t acc = 0;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const uint4 v = row[gr * NQ + q];
-                    acc += v.x + v.y + v.z + v.w;
-                    row[gr * NQ + q] = make_uint4(0, 0, 0, 0);
-                }
-                tot[gr * kTileGroupWords + dst] = acc;
-            }
-            if (tid < 256) {
-                int4* cr = reinterpret_cast<int4*>(sm + kTileCorr + tid * 128);
-#pragma unroll
-                for (int kk = 0; kk < NG; ++kk) {
-                    const int gr = (kk + tid) & (NG - 1);
-                    int acc = 0;
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) {
-                        const int4 v = cr[gr * NQ + q];
-                        acc += v.x + v.y + v.z + v.w;
-                        cr[gr * NQ + q] = make_int4(0, 0, 0, 0);
-                    }
-                    reinterpret_cast<int*>(tot)[gr * kTileGroupWords + 264 * 2 + 544 + pad8(tid)] =
-                        acc;
+                for (int jj = 0; jj < 4; ++jj) {
+                    D.ue[jj] = has_up ? qstep(qfrom(C.e[jj]), D.e[jj]) : kNeutral;
+                    D.uo[jj] = has_up ? qstep(qfrom(C.o[jj]), D.o[jj]) : kNeutral;
                 }
             }
+            if (KIND < 2)
+                return;
+            const bool live = j - 2 < G.nrows;
+            uint32_t qre[4], qro[4], qde[4], qdo[4], Be[4], Bo[4];
+            pair_q(C, D.e, D.o, qre, qro, qde, qdo);
+            b_terms(C, qre, qro, qde, qdo, Be, Bo);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                D.ue[jj] = qde[jj];
+                D.uo[jj] = qdo[jj];
+            }
+            const uint32_t Arn = __byte_perm(C.rn, lane4, 0x5504);
+            if (ALIGNED || !F.ragged) {
+                if (live) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_add_imm<kHistAbs + kOffW>(C.A[i], b_of(Be, Bo, i));
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + D.A[i] + kneg);
+                }
+            } else if (live) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const bool real = i <= G.e;
+                    red_add_imm<kHistAbs + kOffW>(C.A[i], real ? b_of(Be, Bo, i) : 0u);
+                    red_inc(real ? C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg : dummy);
+                    red_inc(real ? C.A[i] + D.A[i] + kneg : dummy);
+                }
+            }
+            if (F.edge && live) {
+                if (row_start)
+                    red_add(corr_base + (C.A[0] >> 6), 1u);
+                if (row_end)
+                    red_add(corr_base + (Arn >> 6), 0xFFFFFFFFu);
+            }
+        };
+        using K0 = std::integral_constant<int, 0>;
+        using K1 = std::integral_constant<int, 1>;
+        using K2 = std::integral_constant<int, 2>;
+        using W0 = std::integral_constant<int, 0>;
+        using W1 = std::integral_constant<int, 1>;
+        using NC = std::false_type;
+        using CR = std::true_type;
+        if (P > 4) {
+            step(X, Y, 0, K0{}, W0{}, NC{});
+            step(Y, X, 1, K1{}, W1{}, NC{});
+        } else {
+            if (has_next)
+                N = geo(i0 + stride);
+            step(X, Y, 0, K0{}, W0{}, CR{});
+            step(Y, X, 1, K1{}, W1{}, CR{});
+        }
+        int j = 2;
+        for (; j + 4 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, NC{});
+            step(Y, X, j + 1, K2{}, W1{}, NC{});
+        }
+        if (has_next)
+            N = geo(i0 + stride);
+        for (; j + 1 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, CR{});
+            step(Y, X, j + 1, K2{}, W1{}, CR{});
+        }
+        if (j < P)
+            step(X, Y, j, K2{}, W0{}, CR{});
+        // border rows of the image: first row +1, last row -1 (its down pairs
+        // were emitted as equal fakes: the down row was the row itself)
+        if (__any_sync(0xFFFFFFFFu, G.nrows > 0 && (G.y0 == 0 || G.y0 + G.nrows == p.h))) {
+            const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
+            if (G.nrows > 0 && G.y0 == 0) {
+                const uint8_t* rp = G.p + p.pitch;
+                for (int i = 0; i < nreal; ++i)
+                    red_add(corr_g + ((uint32_t)rp[i] << 2), 1u);
+            }
+            if (G.nrows > 0 && G.y0 + G.nrows == p.h) {
+                const uint8_t* rp = G.p + (size_t)G.nrows * p.pitch;
+                for (int i = 0; i < nreal; ++i)
+                    red_add(corr_g + ((uint32_t)rp[i] << 2), 0xFFFFFFFFu);
+            }
         }
         __syncthreads();
-#ifdef KOHLER_PHASES
-        { const unsigned long long t = clock64(); t_red += t - t_mark; t_mark = t; }
-#endif
         if (!waited) {
-            pdl_wait();  // the previous launch may still read our output buffers
+            pdl_wait();  // the previous launch may still read our outputs
             waited = true;
         }
-        if (warp < NG && i0 + warp < p.n) {
-            // one warp per image: exact int64 scans -> curve (K3); the next
-            // round's accumulation of the other warps overlaps this
-            const uint32_t* H = tot + warp * kTileGroupWords;  // hist
-            const uint32_t* Q = H + 264;                       // hhi
-            const uint32_t* S = H + 2 * 264;                   // hs
-            const int* Cc = reinterpret_cast<const int*>(H + 2 * 264 + 544);  // corr
-            const long long im = i0 + warp;
-            uint64_t card[8], sum[8];
-            warp_curve256_regs(
-                [&](int x) {
-                    const int px = pad8(x);
-                    return 4ll * H[px] - Cc[px] - 2ll * Q[px];
-                },
-                [&](int u) -> long long {
-                    if (u == 0)
-                        return 0;
-                    const int pm = pad8(u - 1);
-                    long long r2 = 4ll * H[pm] - Cc[pm] - 2ll * S[pad16(2 * u - 2)] -
-                                   (long long)S[pad16(2 * u - 1)];
-                    if (u >= 2)
-                        r2 -= (long long)S[pad16(2 * u - 3)];
-                    return r2;
-                },
-                card, sum);
-            uint64_t* os = p.sums + (size_t)im * 256 + lane * 8;
-            uint64_t* oc = p.cards + (size_t)im * 256 + lane * 8;
+        {
+            // 1. every thread: 2*NG (half-row, group) cells, contiguous 16-byte
+            //    pieces across a warp (conflict free): read, sum the group's LG
+            //    lane words (fields for W), clear
+            constexpr int PER = 1024 * NG / kWalkThreads;
+            uint32_t va[PER], vb[PER];
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                *reinterpret_cast<ulonglong2*>(os + j) = make_ulonglong2(sum[j], sum[j + 1]);
-                *reinterpret_cast<ulonglong2*>(oc + j) = make_ulonglong2(card[j], card[j + 1]);
+            for (int q = 0; q < PER; ++q) {
+                const int idx = tid + kWalkThreads * q;
+                const int rh = idx / NG, gg = idx % NG;
+                uint32_t a = 0, b = 0;
+#pragma unroll
+                for (int q4 = 0; q4 < LG / 4; ++q4) {
+                    uint4* cell = reinterpret_cast<uint4*>(hist + rh * 128 + gg * LG * 4 + 16 * q4);
+                    const uint4 v = *cell;
+                    if (rh & 1) {  // W word: hist | B << 16
+                        a += (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
+                        b += (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
+                    } else {
+                        a += v.x + v.y + v.z + v.w;
+                    }
+                    *cell = make_uint4(0, 0, 0, 0);
+                }
+                va[q] = a;
+                vb[q] = b;
             }
+            __syncthreads();
+            // 2. per-image totals into a padded scratch carved out of the (now
+            //    zero) counter block: hs[s] at s + s/16, the other arrays at
+            //    x + x/8 (conflict-free lane-blocked reads of warp_curve256)
+            uint32_t* scr = reinterpret_cast<uint32_t*>(hist);
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int idx = tid + kWalkThreads * q;
+                const int rh = idx / NG, gg = idx % NG;
+                const int row = rh >> 1;
+                uint32_t* base = scr + gg * kTwImgWords;
+                if (rh & 1) {
+                    const int key = row & 255, cp = row >> 8;
+                    base[kTwH + cp * 2 * kTwArr + pad8(key)] = va[q];
+                    base[kTwH + cp * 2 * kTwArr + kTwArr + pad8(key)] = vb[q];
+                } else {
+                    base[pad16(row)] = va[q];
+                }
+            }
+            __syncthreads();
+            if (warp < NG && i0 + warp < p.n) {
+                // 3. K3 for image i0 + warp
+                const uint32_t* base = scr + warp * kTwImgWords;
+                const uint32_t* h0 = base + kTwH;
+                const uint32_t* b0 = h0 + kTwArr;
+                const uint32_t* h1 = b0 + kTwArr;
+                const uint32_t* b1 = h1 + kTwArr;
+                const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + warp * 1024);
+                auto histv = [&](int v) { return (long long)h0[pad8(v)] + (long long)h1[pad8(v)]; };
+                auto hs = [&](int s) { return (long long)base[pad16(s)]; };
+                uint64_t card[8], sum[8];
+                warp_curve256_regs(
+                    [&](int t) {
+                        return (long long)b0[pad8(t)] + (long long)b1[pad8(t)] - 4ll * histv(t);
+                    },
+                    [&](int u) -> long long {
+                        if (u == 0)
+                            return 0;
+                        long long r2 = 4ll * histv(u - 1) - (long long)cr[u - 1] -
+                                       2ll * hs(2 * u - 2) - hs(2 * u - 1);
+                        if (u >= 2)
+                            r2 -= hs(2 * u - 3);
+                        return r2;
+                    },
+                    card, sum);
+                const long long im = i0 + warp;
+                uint64_t* os = p.sums + (size_t)im * 256 + lane * 8;
+                uint64_t* oc = p.cards + (size_t)im * 256 + lane * 8;
+#pragma unroll
+                for (int jj = 0; jj < 8; jj += 2) {
+                    *reinterpret_cast<ulonglong2*>(os + jj) = make_ulonglong2(sum[jj], sum[jj + 1]);
+                    *reinterpret_cast<ulonglong2*>(oc + jj) = make_ulonglong2(card[jj], card[jj + 1]);
+                }
+            }
+            __syncthreads();
+            // 4. clear the scratch and the border terms for the next round
+            uint4* z = reinterpret_cast<uint4*>(hist);
+            for (int i = tid; i < NG * kTwImgWords / 4; i += kWalkThreads)
+                z[i] = make_uint4(0, 0, 0, 0);
+            for (int i = tid; i < NG * 256; i += kWalkThreads)
+                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
+        __syncthreads();
+        pos += (uint32_t)P;
+        G = N;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (!waited)
         pdl_wait();
     pdl_trigger();
-#ifdef KOHLER_PHASES
-    if (tid == 0 && blockIdx.x < 2048) {
-        g_phase[blockIdx.x][0] = t_acc;
-        g_phase[blockIdx.x][1] = t_red;
-        g_phase[blockIdx.x][2] = clock64() - t_mark;
-    }
-#endif
 }
 
 // Definition-level oracle kernel: block t scans every
@@ -1451,41 +1580,61 @@ int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t str
     return KOHLER_OK;
 }
 
-template <bool VEC, int LG>
-int launch_tile_t(kohler_cuda_ctx* ctx, const TileParams& tp, unsigned G, cudaStream_t stream)
+template <bool ALIGNED, int LG>
+int launch_twalk_t(const TwParams& tp, unsigned G, cudaStream_t stream)
 {
     static bool attr_set = false;  // per process; the attribute is per function
     if (!attr_set) {
-        KC_CUDA(cudaFuncSetAttribute(tile_kernel<VEC, true, LG>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
-        KC_CUDA(cudaFuncSetAttribute(tile_kernel<VEC, false, LG>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+        KC_CUDA(cudaFuncSetAttribute(twalk_kernel<ALIGNED, LG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         attr_set = true;
     }
-    if (tp.w % 16 == 0)
-        KC_CUDA(launch_pdl(tile_kernel<VEC, true, LG>, G, kWideThreads, kTileBytes, stream, tp));
-    else
-        KC_CUDA(launch_pdl(tile_kernel<VEC, false, LG>, G, kWideThreads, kTileBytes, stream, tp));
+    KC_CUDA(launch_pdl(twalk_kernel<ALIGNED, LG>, G, kWalkThreads, kSmWideBytes, stream, tp));
     return KOHLER_OK;
 }
 
-// Batches of small images: K5 tile_kernel (curves) + select_kernel (K4).
+// K5 geometry for a batch of n w x h images: the smallest lane group LG (most
+// images per round) whose 16 * LG walkers cover the image with walks of
+// R <= 62 rows (a W lane word takes <= 16 warps * (R/2 + 1) * 16 <= 8191
+// events per round).  Returns false when no LG fits (K1 is used instead).
+bool twalk_geometry(int n, int w, int h, int& lg, int& R, int& C)
+{
+    const int S = (w + 15) / 16;
+    for (int cand = 4; cand <= 32; cand *= 2) {
+        if (32 / cand > n && cand < 32)
+            continue;  // fewer images than groups: use bigger groups
+        const int walkers = kWalkWarps * cand;
+        if (S > walkers)
+            continue;
+        const int c = walkers / S;
+        const int r = (h + c - 1) / c;
+        if (r > 62)
+            continue;
+        lg = cand;
+        R = r;
+        C = (h + r - 1) / r;
+        return true;
+    }
+    return false;
+}
+
+// Batches of small images: K5 twalk_kernel (curves) + select_kernel (K4).
 int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
                 size_t image_stride, int k, int select, const BatchOut& o, cudaStream_t stream)
 {
-    int ng = 8;
-    while (ng > 1 && ng > n)
-        ng >>= 1;
-    const int lg = 32 / ng;
-    TileParams tp{};
+    int lg = 0, R = 0, C = 0;
+    if (!twalk_geometry(n, w, h, lg, R, C))
+        return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select, o, stream);
+    TwParams tp{};
     tp.px = px;
     tp.pitch = pitch;
     tp.image_stride = image_stride;
     tp.n = n;
     tp.w = w;
     tp.h = h;
-    tp.nseg = (w + 15) / 16;
-    tp.segs = h * tp.nseg;
+    tp.S = (w + 15) / 16;
+    tp.R = R;
+    tp.C = C;
     tp.sums = o.sums;
     tp.cards = o.cards;
     if (!tp.sums) {
@@ -1495,20 +1644,42 @@ int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, si
         tp.sums = static_cast<uint64_t*>(ctx->curves.p);
         tp.cards = tp.sums + (size_t)n * 256;
     }
-    const long long groups = (n + ng - 1) / ng;
-    const unsigned G = (unsigned)std::max(1ll, std::min<long long>(groups, ctx->sm_count));
     const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
                      (image_stride % 16 == 0);
+    if (!vec) {
+        // cp.async reads 16-byte segments: stage unaligned inputs
+        const size_t dpitch = round_up((size_t)w, 16);
+        const size_t dstride = dpitch * (size_t)h;
+        int rc = ctx->stage.ensure(dstride * (size_t)n);
+        if (rc)
+            return rc;
+        uint8_t* d = static_cast<uint8_t*>(ctx->stage.p);
+        if (image_stride == pitch * (size_t)h) {
+            KC_CUDA(cudaMemcpy2DAsync(d, dpitch, px, pitch, (size_t)w, (size_t)h * n,
+                                      cudaMemcpyDeviceToDevice, stream));
+        } else {
+            for (int i = 0; i < n; ++i)
+                KC_CUDA(cudaMemcpy2DAsync(d + dstride * i, dpitch, px + image_stride * i, pitch,
+                                          (size_t)w, (size_t)h, cudaMemcpyDeviceToDevice, stream));
+        }
+        tp.px = d;
+        tp.pitch = dpitch;
+        tp.image_stride = dstride;
+    }
+    const int ng = 32 / lg;
+    const long long rounds = (n + ng - 1) / ng;
+    const unsigned G = (unsigned)std::max(1ll, std::min<long long>(rounds, ctx->sm_count - 1));
+    const bool aligned = w % 16 == 0;
     int rc = KOHLER_OK;
-    switch (lg * 2 + (vec ? 1 : 0)) {
-    case 4 * 2 + 1: rc = launch_tile_t<true, 4>(ctx, tp, G, stream); break;
-    case 4 * 2: rc = launch_tile_t<false, 4>(ctx, tp, G, stream); break;
-    case 8 * 2 + 1: rc = launch_tile_t<true, 8>(ctx, tp, G, stream); break;
-    case 8 * 2: rc = launch_tile_t<false, 8>(ctx, tp, G, stream); break;
-    case 16 * 2 + 1: rc = launch_tile_t<true, 16>(ctx, tp, G, stream); break;
-    case 16 * 2: rc = launch_tile_t<false, 16>(ctx, tp, G, stream); break;
-    case 32 * 2 + 1: rc = launch_tile_t<true, 32>(ctx, tp, G, stream); break;
-    default: rc = launch_tile_t<false, 32>(ctx, tp, G, stream); break;
+    switch (lg * 2 + (aligned ? 1 : 0)) {
+    case 4 * 2 + 1: rc = launch_twalk_t<true, 4>(tp, G, stream); break;
+    case 4 * 2: rc = launch_twalk_t<false, 4>(tp, G, stream); break;
+    case 8 * 2 + 1: rc = launch_twalk_t<true, 8>(tp, G, stream); break;
+    case 8 * 2: rc = launch_twalk_t<false, 8>(tp, G, stream); break;
+    case 16 * 2 + 1: rc = launch_twalk_t<true, 16>(tp, G, stream); break;
+    case 16 * 2: rc = launch_twalk_t<false, 16>(tp, G, stream); break;
+    case 32 * 2 + 1: rc = launch_twalk_t<true, 32>(tp, G, stream); break;
+    default: rc = launch_twalk_t<false, 32>(tp, G, stream); break;
     }
     if (rc)
         return rc;
