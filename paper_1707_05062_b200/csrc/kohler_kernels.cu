@@ -1253,6 +1253,67 @@ __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
         p.status[cidx] = st;
 }
 
+// Standalone selection for 256-level curves: one warp per curve, 8 curves per
+// CTA, lane L holding thresholds 8L..8L+7 in registers (vector loads), the
+// register-resident selection of kohler_walk.cuh.
+__global__ void __launch_bounds__(256) select256_kernel(const SelectParams p)
+{
+    __shared__ double smv[8][128];
+    __shared__ int smt[8][128];
+    pdl_wait();  // curves may come from the preceding (PDL-overlapped) launch
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const long long cidx = (long long)blockIdx.x * 8 + wq;
+    if (cidx >= p.n_curves)
+        return;
+    const size_t off = (size_t)cidx * 256 + 8 * lane;
+    double v[8];
+    bool d[8];
+    if (p.sums) {
+        uint64_t s[8], c[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+            const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(p.sums + off + j);
+            const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(p.cards + off + j);
+            s[j] = a.x;
+            s[j + 1] = a.y;
+            c[j] = b.x;
+            c[j + 1] = b.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            d[j] = c[j] != 0;
+            v[j] = d[j] ? (double)s[j] / (double)c[j] : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = p.in_values[off + j];
+            d[j] = p.in_defined[off + j] != 0;
+        }
+    }
+    if (p.values) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2)
+            *reinterpret_cast<double2*>(p.values + off + j) = make_double2(v[j], v[j + 1]);
+    }
+    if (p.defined) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            lo |= (d[j] ? 1u : 0u) << (8 * j);
+            hi |= (d[j + 4] ? 1u : 0u) << (8 * j);
+        }
+        *reinterpret_cast<uint2*>(p.defined + off) = make_uint2(lo, hi);
+    }
+    if (!p.want_select)
+        return;
+    const int st = kohler_walk::warp_select256_regs(
+        v, d, p.k, smv[wq], smt[wq], p.t0s ? p.t0s + cidx : nullptr,
+        p.topks ? p.topks + (size_t)cidx * p.k : nullptr, p.topk_counts ? p.topk_counts + cidx : nullptr);
+    if (lane == 0 && p.status)
+        p.status[cidx] = st;
+}
+
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -1569,6 +1630,11 @@ int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t str
 {
     if (sp.n_curves == 0)
         return KOHLER_OK;
+    if (sp.levels == 256) {
+        KC_CUDA(launch_pdl(select256_kernel, (unsigned)((sp.n_curves + 7) / 8), 256, 0, stream, sp));
+        ctx->last_launches += 1;
+        return KOHLER_OK;
+    }
     const size_t smem = (size_t)sp.levels * (8 * 3 + 4 * 2 + 1);
     if (!ctx->select_attr_set) {
         KC_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
