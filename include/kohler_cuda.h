@@ -22,6 +22,13 @@
  *   kohler_cuda_analyze[_batch]  -> the per-image pipeline curve -> mean_contrast ->
  *                                   optimal_threshold -> top_k_local_maxima of
  *                                   tools/kohler_main.cpp:91-107 and src/bench.cpp:263-277
+ *   kohler_cuda_classify         -> kohler::classify (threshold.hpp:62-64, src/threshold.cpp:84-101)
+ *   kohler_cuda_quantize         -> kohler::quantize (threshold.hpp:66-67, src/threshold.cpp:103-126)
+ *   kohler_cuda_segment_batch[_device] -> the per-frame video pipeline of
+ *                                   src/bench.cpp:266-281 (curve -> {t0} -> two-class
+ *                                   quantize, pass-through without boundary) and, with
+ *                                   k >= 1, the segment command's top-k quantize
+ *                                   (tools/kohler_main.cpp:91-103)
  *
  * Results are bit-identical to the reference: integer curves exactly, the
  * double curve bit-for-bit (IEEE division of exactly-representable operands),
@@ -136,6 +143,33 @@ int kohler_cuda_select_device(kohler_cuda_ctx *ctx, const uint64_t *sums,
 
 /* Number of kernels the last call on this context launched (bench evidence). */
 int kohler_cuda_last_launch_count(const kohler_cuda_ctx *ctx);
+
+/* label[i] = number of thresholds strictly below px[i] (thresholds sorted
+ * ascending, as a ThresholdSet holds them; nts >= 0).  Host buffers; labels
+ * is w*h bytes, row-major without padding. */
+int kohler_cuda_classify(kohler_cuda_ctx *ctx, const uint8_t *px, int w, int h, size_t pitch,
+                         const int *thresholds, int nts, uint8_t *labels);
+
+/* out[i] = mean grey value of px[i]'s class, rounded half up (classes by
+ * kohler_cuda_classify).  Host buffers; out is w*h bytes, row-major. */
+int kohler_cuda_quantize(kohler_cuda_ctx *ctx, const uint8_t *px, int w, int h, size_t pitch,
+                         const int *thresholds, int nts, uint8_t *out);
+
+/* Per-image segmentation of a batch: k == 0: the video pipeline (threshold
+ * set {optimal_threshold}, two classes); k >= 1: top_k_local_maxima(k).
+ * Images without boundary are copied through unchanged and get status 1
+ * (KOHLER_NO_BOUNDARY), ts_counts 0.  thresholds: [n][max(k,1)] ints.
+ * Device pointers, asynchronous on `stream`. */
+int kohler_cuda_segment_batch_device(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w,
+                                     int h, size_t pitch, size_t image_stride, int k,
+                                     uint8_t *out, size_t out_pitch, size_t out_stride,
+                                     int *thresholds, int *ts_counts, int *status,
+                                     void *stream);
+
+/* Same on host buffers (row-major, no padding); blocks until done. */
+int kohler_cuda_segment_batch(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w, int h,
+                              int k, uint8_t *out, int *thresholds, int *ts_counts,
+                              int *status);
 
 #ifdef __cplusplus
 }

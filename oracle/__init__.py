@@ -174,6 +174,9 @@ class Reference:
             ("kref_pipeline", [vp, u, i, vp, vp, vp, vp, vp, vp, vp], i),
             ("kref_pipeline_batch", [vp, i, u, i, i, vp, vp, vp, vp, vp], i),
             ("kref_time_pipeline", [vp, u, i, i, i], C.c_double),
+            ("kref_classify", [vp, vp, i, vp], None),
+            ("kref_quantize", [vp, vp, i, vp], None),
+            ("kref_segment", [vp, u, i, vp, vp, vp], i),
         ]:
             f = getattr(self.lib, name)
             f.argtypes = args
@@ -264,6 +267,39 @@ class Reference:
         for hh in handles:
             hh.close()
         return dict(sums=sums, cards=cards, t0=t0, topk=tk, topk_count=cnt)
+
+
+def _ref_thresholds(ts):
+    return np.ascontiguousarray(np.asarray(ts, dtype=np.int32).reshape(-1))
+
+
+def ref_classify(ref, img, ts):
+    """Reference classify (threshold.cpp:84-101) -> u8 labels, same shape."""
+    t = _ref_thresholds(ts)
+    out = np.zeros(img.shape, np.uint8)
+    with RefImage(ref, img) as im:
+        ref.lib.kref_classify(im.h, _p(t), t.shape[0], _p(out))
+    return out
+
+
+def ref_quantize(ref, img, ts):
+    """Reference quantize (threshold.cpp:103-126) -> u8 image."""
+    t = _ref_thresholds(ts)
+    out = np.zeros(img.shape, np.uint8)
+    with RefImage(ref, img) as im:
+        ref.lib.kref_quantize(im.h, _p(t), t.shape[0], _p(out))
+    return out
+
+
+def ref_segment(ref, img, k=0, workers=1):
+    """One frame of the reference video pipeline (bench.cpp:266-281; k > 0:
+    the segment command's top-k).  -> (out image, thresholds, status)."""
+    out = np.zeros(img.shape, np.uint8)
+    ts = np.zeros(max(k, 1), np.int32)
+    cnt = np.zeros(1, np.int32)
+    with RefImage(ref, img) as im:
+        st = ref.lib.kref_segment(im.h, int(workers), int(k), _p(out), _p(ts), _p(cnt))
+    return out, list(ts[:int(cnt[0])]), int(st)
 
 
 class RefImage:

@@ -236,3 +236,56 @@ double kref_time_pipeline(const void* img, unsigned workers, int k, int warmup, 
 }
 
 } // extern "C"
+
+extern "C" {
+
+// classify / quantize (proj/src/threshold.cpp:84-126) with a given set of
+// thresholds (sorted, as a ThresholdSet holds them).
+void kref_classify(const void* img, const int* ts, int nts, uint8_t* labels)
+{
+    kohler::ThresholdSet s;
+    s.thresholds.assign(ts, ts + nts);
+    const auto l = kohler::classify(*static_cast<const kohler::GrayImage*>(img), s);
+    std::copy(l.labels.begin(), l.labels.end(), labels);
+}
+
+void kref_quantize(const void* img, const int* ts, int nts, uint8_t* out)
+{
+    kohler::ThresholdSet s;
+    s.thresholds.assign(ts, ts + nts);
+    const auto q = kohler::quantize(*static_cast<const kohler::GrayImage*>(img), s);
+    const auto px = q.pixels();
+    std::copy(px.begin(), px.end(), out);
+}
+
+// One video frame of proj/src/bench.cpp:266-281: curve -> mean -> {t0} ->
+// two-class quantize; a frame without boundary passes through unchanged.
+// k > 0: the segment command's top-k thresholds (tools/kohler_main.cpp:95-103)
+// instead of {t0}.  Returns 1 for a frame without boundary, else 0.
+int kref_segment(const void* img, unsigned workers, int k, uint8_t* out, int* ts_out,
+                 int* ts_count)
+{
+    const auto& im = *static_cast<const kohler::GrayImage*>(img);
+    const kohler::ContrastCurve c = kohler::fast_contrast_curve(im, workers);
+    *ts_count = 0;
+    try {
+        const kohler::MeanContrastCurve mc = kohler::mean_contrast(c);
+        kohler::ThresholdSet ts;
+        if (k <= 0)
+            ts.thresholds.push_back(kohler::optimal_threshold(mc));
+        else
+            ts = kohler::top_k_local_maxima(mc, k);
+        const auto q = kohler::quantize(im, ts);
+        const auto px = q.pixels();
+        std::copy(px.begin(), px.end(), out);
+        *ts_count = static_cast<int>(ts.thresholds.size());
+        std::copy(ts.thresholds.begin(), ts.thresholds.end(), ts_out);
+        return 0;
+    } catch (const kohler::NoBoundaryError&) {
+        const auto px = im.pixels();
+        std::copy(px.begin(), px.end(), out);
+        return 1;
+    }
+}
+
+} // extern "C"

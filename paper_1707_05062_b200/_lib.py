@@ -51,6 +51,11 @@ SIGNATURES = {
     "kohler_cuda_select_device": (
         _i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kohler_cuda_last_launch_count": (_i, [_vp]),
+    "kohler_cuda_classify": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
+    "kohler_cuda_quantize": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
+    "kohler_cuda_segment_batch_device": (
+        _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _sz, _sz, _vp, _vp, _vp, _vp]),
+    "kohler_cuda_segment_batch": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
 }
 
 _lock = threading.Lock()

@@ -16,6 +16,9 @@ mean_contrast              threshold.hpp:50 / threshold.cpp:9-23          kohler
 optimal_threshold          threshold.hpp:54 / threshold.cpp:25-37         kohler_cuda_optimal_threshold
 top_k_local_maxima         threshold.hpp:60 / threshold.cpp:39-82         kohler_cuda_top_k_local_maxima
 NoBoundaryError            threshold.hpp:14-20                            KOHLER_NO_BOUNDARY
+LabelImage                 threshold.hpp:40-48                            (host array)
+classify                   threshold.hpp:62-64 / threshold.cpp:84-101     kohler_cuda_classify
+quantize                   threshold.hpp:66-67 / threshold.cpp:103-126    kohler_cuda_quantize
 =========================  =============================================  ======================
 
 Plus the batched / device-resident entry points of the B200 build
@@ -277,6 +280,54 @@ class Context:
             _stream(stream)))
 
 
+    # ---- segmentation -------------------------------
+    def classify(self, px: np.ndarray, thresholds) -> np.ndarray:
+        """labels[y, x] = number of thresholds strictly below px[y, x]."""
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        h, w = px.shape
+        ts = np.ascontiguousarray(np.asarray(thresholds, dtype=np.int32).reshape(-1))
+        out = np.empty((h, w), np.uint8)
+        _raise_for(self._lib.kohler_cuda_classify(self._h, _ptr(px), w, h, w, _ptr(ts),
+                                                  ts.shape[0], _ptr(out)))
+        return out
+
+    def quantize(self, px: np.ndarray, thresholds) -> np.ndarray:
+        """Each pixel replaced by its class mean, rounded half up."""
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        h, w = px.shape
+        ts = np.ascontiguousarray(np.asarray(thresholds, dtype=np.int32).reshape(-1))
+        out = np.empty((h, w), np.uint8)
+        _raise_for(self._lib.kohler_cuda_quantize(self._h, _ptr(px), w, h, w, _ptr(ts),
+                                                  ts.shape[0], _ptr(out)))
+        return out
+
+    def segment_batch(self, px: np.ndarray, k: int = 0):
+        """Per-image segmentation of px[n, h, w]: k == 0 the video pipeline
+        (bench.cpp:266-281: {optimal_threshold}, two classes), k >= 1 the
+        top-k quantize of the segment command.  Frames without boundary pass
+        through (status 1).  -> (out[n, h, w], thresholds[n, max(k,1)],
+        counts[n], status[n])."""
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        if px.ndim == 2:
+            px = px[None]
+        n, h, w = px.shape
+        out = np.empty_like(px)
+        ts = np.zeros((n, max(k, 1)), np.int32)
+        cnt = np.zeros(n, np.int32)
+        st = np.zeros(n, np.int32)
+        _raise_for(self._lib.kohler_cuda_segment_batch(self._h, _ptr(px), n, w, h, int(k),
+                                                       _ptr(out), _ptr(ts), _ptr(cnt), _ptr(st)))
+        return out, ts, cnt, st
+
+    def segment_batch_device(self, px, w: int, h: int, pitch: int, image_stride: int, n: int,
+                             k: int, out, out_pitch: int, out_stride: int, thresholds, counts,
+                             status, stream=None) -> None:
+        _raise_for(self._lib.kohler_cuda_segment_batch_device(
+            self._h, _dptr(px), int(n), int(w), int(h), int(pitch), int(image_stride), int(k),
+            _dptr(out), int(out_pitch), int(out_stride), _dptr(thresholds), _dptr(counts),
+            _dptr(status), _stream(stream)))
+
+
 def _alloc_result(n: int, k: int, curves: bool, mean: bool) -> BatchResult:
     return BatchResult(
         sums=np.zeros((n, LEVELS), np.uint64) if curves else None,
@@ -377,3 +428,33 @@ def top_k_local_maxima(mc: MeanContrastCurve, k: int) -> ThresholdSet:
 
 def analyze_batch(px: np.ndarray, k: int = 6) -> BatchResult:
     return default_context().analyze_batch(px, k)
+
+
+@dataclass
+class LabelImage:
+    """Class index per pixel (reference: kohler::LabelImage, threshold.hpp:40-48)."""
+    width: int
+    height: int
+    labels: np.ndarray
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, LabelImage) and self.width == other.width and
+                self.height == other.height and np.array_equal(self.labels, other.labels))
+
+
+def _ts_list(ts) -> list:
+    return list(ts.thresholds) if isinstance(ts, ThresholdSet) else list(ts)
+
+
+def classify(img, ts) -> LabelImage:
+    """label(x) = number of thresholds strictly below the pixel value
+    (threshold.cpp:84-101), on the GPU."""
+    a = _as_array(img)
+    return LabelImage(a.shape[1], a.shape[0], default_context().classify(a, _ts_list(ts)))
+
+
+def quantize(img, ts) -> GrayImage:
+    """Every pixel replaced by the mean grey value of its class, rounded half
+    up (threshold.cpp:103-126), on the GPU."""
+    a = _as_array(img)
+    return GrayImage.from_array(default_context().quantize(a, _ts_list(ts)))

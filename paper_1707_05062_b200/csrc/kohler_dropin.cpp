@@ -8,6 +8,8 @@
 //   mean_contrast         -> kohler_cuda_mean_contrast  (ref src/threshold.cpp:9-23)
 //   optimal_threshold     -> kohler_cuda_optimal_threshold (ref :25-37)
 //   top_k_local_maxima    -> kohler_cuda_top_k_local_maxima (ref :39-82)
+//   classify              -> kohler_cuda_classify       (ref :84-101)
+//   quantize              -> kohler_cuda_quantize       (ref :103-126)
 // pair_contribution / merge_accumulators are the reference's tiny host
 // utilities (ref src/curve.cpp:10-30) and stay on the host.
 //
@@ -161,6 +163,27 @@ ThresholdSet top_k_local_maxima(const MeanContrastCurve& mc, int k)
                                              &count));
     out.resize(static_cast<std::size_t>(count));
     return ThresholdSet{std::move(out)};
+}
+
+LabelImage classify(const GrayImage& img, const ThresholdSet& ts)
+{
+    LabelImage out{img.width(), img.height(), {}};
+    out.labels.resize(img.pixel_count());
+    const auto px = img.pixels();
+    raise_for(kohler_cuda_classify(context(), px.data(), img.width(), img.height(),
+                                   static_cast<std::size_t>(img.width()), ts.thresholds.data(),
+                                   static_cast<int>(ts.thresholds.size()), out.labels.data()));
+    return out;
+}
+
+GrayImage quantize(const GrayImage& img, const ThresholdSet& ts)
+{
+    GrayImage out(img.width(), img.height());
+    const auto px = img.pixels();
+    raise_for(kohler_cuda_quantize(context(), px.data(), img.width(), img.height(),
+                                   static_cast<std::size_t>(img.width()), ts.thresholds.data(),
+                                   static_cast<int>(ts.thresholds.size()), out.pixels().data()));
+    return out;
 }
 
 } // namespace kohler

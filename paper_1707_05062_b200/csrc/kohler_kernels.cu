@@ -61,6 +61,7 @@ struct WideParams {
     int k;
     int select;
     int no_finish;  // accumulate only (a band of a chunked image; a later launch finishes)
+    uint32_t* hist_out;  // [n][256] pixel histogram (atomically accumulated), or null
     uint64_t* sums;
     uint64_t* cards;
     double* values;
@@ -310,6 +311,11 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
         if (val != 0) {
             const int copy = blockIdx.x % p.copies;
             atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + t, (unsigned long long)val);
+        }
+        if (p.hist_out && t < 256) {
+            const uint32_t hv = (uint32_t)hist(t);  // the W words' pixel counts
+            if (hv)
+                atomicAdd(p.hist_out + (size_t)img * 256 + t, hv);
         }
     }
     __syncthreads();
@@ -828,6 +834,7 @@ struct TwParams {
     int C;  // walk chunks per image (S * C <= 16 * LG)
     uint64_t* sums;
     uint64_t* cards;
+    uint32_t* hist_out;  // [n][256] pixel histogram, or null
 };
 
 // K5 per-image totals scratch (u32, padded): hs[512] at pad16, then
@@ -1125,6 +1132,11 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
                     *reinterpret_cast<ulonglong2*>(os + jj) = make_ulonglong2(sum[jj], sum[jj + 1]);
                     *reinterpret_cast<ulonglong2*>(oc + jj) = make_ulonglong2(card[jj], card[jj + 1]);
                 }
+                if (p.hist_out) {
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        p.hist_out[(size_t)im * 256 + lane * 8 + jj] = (uint32_t)histv(lane * 8 + jj);
+                }
             }
             __syncthreads();
             // 4. clear the scratch and the border terms for the next round
@@ -1315,6 +1327,258 @@ __global__ void __launch_bounds__(256) select256_kernel(const SelectParams p)
 }
 
 // ---------------------------------------------------------------------------
+// Segmentation: classify / quantize
+// (proj/src/threshold.cpp:84-126) and the per-frame video pipeline
+// (proj/src/bench.cpp:266-281).  hist_kernel: pixel histogram per image
+// (lane-striped shared counters, only needed when no K1 ran); map_kernel:
+// per image a 256-entry LUT (label = #thresholds < v, or the class mean
+// rounded half up from the histogram, or identity for a frame without
+// boundary), then one pass out = LUT[in].
+// ---------------------------------------------------------------------------
+struct MapParams {
+    const uint8_t* px;
+    size_t pitch, image_stride;
+    uint8_t* out;
+    size_t out_pitch, out_stride;
+    int n, w, h;
+    int mode;                 // 0 classify, 1 quantize
+    const int* thresholds;    // [n][ts_stride]; or a single shared set (ts_stride == 0)
+    int ts_stride;
+    const int* ts_counts;     // [n] or null (then ts_count for all)
+    int ts_count;
+    const int* status;        // [n] or null: 1 = no boundary -> pass through
+    const uint32_t* hist;     // [n][256] (quantize)
+    int units_per_image;      // row ranges per image, one warp each
+    int flat;                 // rows dense (pitch == out_pitch == w, w % 16 == 0), 16-aligned
+    uint32_t seg_magic;       // floor(2^32 / segments per row) + 1
+    int* counts_out;          // [n] or null: thresholds applied per image (0 if passed through)
+};
+
+// q = i / d for 0 <= i < 2^31 / d via multiply-high (magic = floor(2^32 / d) + 1)
+__device__ __forceinline__ uint32_t div_magic(uint32_t i, uint32_t magic, uint32_t d)
+{
+    return d == 1 ? i : __umulhi(i, magic);
+}
+
+__global__ void __launch_bounds__(512) hist_kernel(const uint8_t* px, size_t pitch,
+                                                   size_t image_stride, int w, int h,
+                                                   int blocks_per_image, uint32_t magic,
+                                                   uint32_t* hist)
+{
+    __shared__ uint32_t sh[256 * 32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < 256 * 32; i += 512)
+        sh[i] = 0;
+    __syncthreads();
+    const int img = blockIdx.x / blocks_per_image, b = blockIdx.x % blocks_per_image;
+    const int y0 = (int)((long long)h * b / blocks_per_image);
+    const int y1 = (int)((long long)h * (b + 1) / blocks_per_image);
+    const uint8_t* base = px + (size_t)img * image_stride;
+    const uint32_t segs = (uint32_t)(w + 15) / 16;
+    const uint32_t total = (uint32_t)(y1 - y0) * segs;
+    for (uint32_t i = tid; i < total; i += 512) {
+        const uint32_t q = div_magic(i, magic, segs);
+        const int y = y0 + (int)q, s = (int)(i - q * segs);
+        const uint8_t* rp = base + (size_t)y * pitch + 16 * s;
+        const int nb = min(16, w - 16 * s);
+        if (nb == 16 && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(rp));
+            const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                atomicAdd(&sh[((wd[j >> 2] >> (8 * (j & 3))) & 0xFFu) * 32 + lane], 1u);
+        } else {
+            for (int j = 0; j < nb; ++j)
+                atomicAdd(&sh[(uint32_t)rp[j] * 32 + lane], 1u);
+        }
+    }
+    __syncthreads();
+    if (tid < 256) {
+        uint32_t s = 0;
+        for (int l = 0; l < 32; ++l)
+            s += sh[tid * 32 + ((l + tid) & 31)];
+        if (s)
+            atomicAdd(hist + (size_t)img * 256 + tid, s);
+    }
+}
+
+// One warp per unit (an image, or a row range of a large one): the warp builds
+// its image's LUT from the histogram with shuffles (no block barriers), then
+// streams its rows with kMapUnroll 16-byte loads in flight per lane.
+constexpr int kMapWarps = 8, kMapThreads = 32 * kMapWarps, kMapUnroll = 8;
+
+struct MapLut {
+    uint32_t y7, ny;      // threshold + 1 replicated per byte: low 7 bits; complement
+    uint32_t m0, mx;      // class-0 byte replicated, class-0 ^ class-1
+    const uint8_t* lut;   // 256 entries (shared)
+};
+
+// KIND 1: two classes, out = v > t ? m1 : m0 per byte (SWAR: borrow-free low-7
+// compare, majority with the top bits, sign-replicating PRMT, select);
+// KIND 2: identity; KIND 0: LUT
+template <int KIND>
+__device__ __forceinline__ uint32_t map_word(uint32_t x, const MapLut& m)
+{
+    if (KIND == 2)
+        return x;
+    if (KIND == 1) {
+        const uint32_t d = (x | 0x80808080u) - m.y7;
+        uint32_t ge, mask;
+        asm("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(ge) : "r"(x), "r"(m.ny), "r"(d));
+        asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(mask) : "r"(ge));
+        return m.m0 ^ (mask & m.mx);
+    }
+    return (uint32_t)m.lut[x & 0xFFu] | ((uint32_t)m.lut[(x >> 8) & 0xFFu] << 8) |
+           ((uint32_t)m.lut[(x >> 16) & 0xFFu] << 16) | ((uint32_t)m.lut[x >> 24] << 24);
+}
+
+template <int KIND>
+__device__ __forceinline__ uint4 map16(uint4 v, const MapLut& m)
+{
+    return make_uint4(map_word<KIND>(v.x, m), map_word<KIND>(v.y, m), map_word<KIND>(v.z, m),
+                      map_word<KIND>(v.w, m));
+}
+
+// rows [y0, y1) of one image by one warp
+template <int KIND>
+__device__ __forceinline__ void map_rows(const MapParams& p, const uint8_t* src, uint8_t* dst,
+                                         int y0, int y1, const MapLut& m, int lane)
+{
+    if (p.flat) {
+        // dense 16-aligned rows: one contiguous range, immediate-offset loads
+        const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)y0 * p.w);
+        uint4* d = reinterpret_cast<uint4*>(dst + (size_t)y0 * p.w);
+        const uint32_t nv = (uint32_t)((size_t)(y1 - y0) * p.w / 16);
+        uint32_t i = lane;
+        for (; i + 32 * (kMapUnroll - 1) < nv; i += 32 * kMapUnroll) {
+            uint4 v[kMapUnroll];
+#pragma unroll
+            for (int u = 0; u < kMapUnroll; ++u)
+                v[u] = __ldg(s + i + 32 * u);
+#pragma unroll
+            for (int u = 0; u < kMapUnroll; ++u)
+                d[i + 32 * u] = map16<KIND>(v[u], m);
+        }
+        for (; i < nv; i += 32)
+            d[i] = map16<KIND>(__ldg(s + i), m);
+        return;
+    }
+    const uint32_t segs = (uint32_t)(p.w + 15) / 16;
+    const uint32_t total = (uint32_t)(y1 - y0) * segs;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | p.pitch |
+                       reinterpret_cast<uintptr_t>(dst) | p.out_pitch) & 15) == 0;
+    for (uint32_t i = lane; i < total; i += 32) {
+        const uint32_t q = div_magic(i, p.seg_magic, segs);
+        const int y = y0 + (int)q, s = (int)(i - q * segs);
+        const uint8_t* rp = src + (size_t)y * p.pitch + 16 * s;
+        uint8_t* wp = dst + (size_t)y * p.out_pitch + 16 * s;
+        const int nb = min(16, p.w - 16 * s);
+        if (nb == 16 && vec)
+            *reinterpret_cast<uint4*>(wp) = map16<KIND>(__ldg(reinterpret_cast<const uint4*>(rp)), m);
+        else
+            for (int j = 0; j < nb; ++j)
+                wp[j] = m.lut[rp[j]];
+    }
+}
+
+__global__ void __launch_bounds__(kMapThreads) map_kernel(const MapParams p)
+{
+    __shared__ unsigned long long pre[kMapWarps][2][256];  // per-warp prefix sums (count, sum)
+    __shared__ uint8_t luts[kMapWarps][256], cmeans[kMapWarps][256];
+    pdl_wait();  // thresholds / histograms come from the preceding launches
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long unit = (long long)blockIdx.x * kMapWarps + wid;
+    if (unit >= (long long)p.n * p.units_per_image)
+        return;  // whole warp; only __syncwarp below
+    const int img = (int)(unit / p.units_per_image), part = (int)(unit % p.units_per_image);
+    uint8_t* lut = luts[wid];
+    const int* ts = p.thresholds + (size_t)img * p.ts_stride;
+    const bool pass = p.status && p.status[img] != 0;
+    const int nts = pass ? 0 : p.ts_counts ? p.ts_counts[img] : p.ts_count;
+    if (p.counts_out && part == 0 && lane == 0)
+        p.counts_out[img] = nts;
+    // label(v) = number of thresholds strictly below v (lower_bound on the
+    // sorted set); class l holds the grey levels (ts[l-1], ts[l]]
+    int label[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        label[j] = 0;
+    for (int i = 0; i < nts; ++i) {
+        const int t = ts[i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            label[j] += t < lane * 8 + j;
+    }
+    if (pass || p.mode == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            lut[lane * 8 + j] = (uint8_t)(pass ? lane * 8 + j : label[j]);
+    } else {
+        const uint4* hp = reinterpret_cast<const uint4*>(p.hist + (size_t)img * 256 + lane * 8);
+        const uint4 h0 = hp[0], h1 = hp[1];
+        const uint32_t hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        unsigned long long pc[8], ps[8], c = 0, s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c += hv[j];
+            s += (unsigned long long)hv[j] * (unsigned)(lane * 8 + j);
+            pc[j] = c;
+            ps[j] = s;
+        }
+        unsigned long long ic = c, is = s;  // inclusive warp scan of the lane totals
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long yc = __shfl_up_sync(0xFFFFFFFFu, ic, off);
+            const unsigned long long ys = __shfl_up_sync(0xFFFFFFFFu, is, off);
+            if (lane >= off) {
+                ic += yc;
+                is += ys;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            pre[wid][0][lane * 8 + j] = pc[j] + ic - c;
+            pre[wid][1][lane * 8 + j] = ps[j] + is - s;
+        }
+        __syncwarp();
+        for (int l = lane; l <= nts; l += 32) {  // one class mean per lane
+            const int lo = l == 0 ? -1 : min(max(ts[l - 1], -1), 255);
+            const int hi = l == nts ? 255 : min(max(ts[l], -1), 255);
+            unsigned long long cs = 0, cc = 0;
+            if (hi > lo) {
+                cc = pre[wid][0][hi] - (lo >= 0 ? pre[wid][0][lo] : 0ull);
+                cs = pre[wid][1][hi] - (lo >= 0 ? pre[wid][1][lo] : 0ull);
+            }
+            cmeans[wid][l] = cc ? (uint8_t)((2 * cs + cc) / (2 * cc)) : 0;  // round half up
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            lut[lane * 8 + j] = cmeans[wid][label[j]];
+    }
+    __syncwarp();
+    MapLut m;
+    m.lut = lut;
+    // two classes: lut[0] / lut[255] are the class values (equal when the
+    // threshold lies outside 0..254, so the compare result does not matter)
+    const int y = min(max((nts >= 1 ? ts[0] : 0) + 1, 0), 255);
+    m.y7 = (uint32_t)(y & 0x7F) * 0x01010101u;
+    m.ny = ~((uint32_t)y * 0x01010101u);
+    m.m0 = (uint32_t)lut[0] * 0x01010101u;
+    m.mx = m.m0 ^ ((uint32_t)lut[255] * 0x01010101u);
+    const int y0 = (int)((long long)p.h * part / p.units_per_image);
+    const int y1 = (int)((long long)p.h * (part + 1) / p.units_per_image);
+    const uint8_t* src = p.px + (size_t)img * p.image_stride;
+    uint8_t* dst = p.out + (size_t)img * p.out_stride;
+    if (pass)
+        map_rows<2>(p, src, dst, y0, y1, m, lane);
+    else if (nts == 1)
+        map_rows<1>(p, src, dst, y0, y1, m, lane);
+    else
+        map_rows<0>(p, src, dst, y0, y1, m, lane);
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
 
@@ -1406,6 +1670,7 @@ struct kohler_cuda_ctx {
     DevBuf curves;   // K5 curve scratch when the caller wants no curves
     DevBuf stage;    // 16-byte aligned copy of unaligned device inputs for K1
     HostBuf hout;    // pinned staging for small results (one D2H per call)
+    DevBuf seg;      // segmentation scratch (histograms, thresholds)
     int last_launches = 0;
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
     bool wide_attr_set = false;
@@ -1473,7 +1738,8 @@ cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, 
 // Launch K1 over n images whose buffers hold band_rows own rows (+ halo).
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
-                const BatchOut& o, cudaStream_t stream, int no_finish = 0)
+                const BatchOut& o, cudaStream_t stream, int no_finish = 0,
+                uint32_t* hist_out = nullptr)
 {
     if (n == 0)
         return KOHLER_OK;
@@ -1548,6 +1814,7 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     p.k = k;
     p.select = select;
     p.no_finish = no_finish;
+    p.hist_out = hist_out;
     p.sums = o.sums;
     p.cards = o.cards;
     p.values = o.values;
@@ -1686,11 +1953,13 @@ bool twalk_geometry(int n, int w, int h, int& lg, int& R, int& C)
 
 // Batches of small images: K5 twalk_kernel (curves) + select_kernel (K4).
 int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
-                size_t image_stride, int k, int select, const BatchOut& o, cudaStream_t stream)
+                size_t image_stride, int k, int select, const BatchOut& o, cudaStream_t stream,
+                uint32_t* hist_out = nullptr)
 {
     int lg = 0, R = 0, C = 0;
     if (!twalk_geometry(n, w, h, lg, R, C))
-        return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select, o, stream);
+        return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select, o, stream, 0,
+                           hist_out);
     TwParams tp{};
     tp.px = px;
     tp.pitch = pitch;
@@ -1703,6 +1972,7 @@ int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, si
     tp.C = C;
     tp.sums = o.sums;
     tp.cards = o.cards;
+    tp.hist_out = hist_out;
     if (!tp.sums) {
         int rc = ctx->curves.ensure((size_t)n * 512 * sizeof(uint64_t));
         if (rc)
@@ -1933,6 +2203,152 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     return KOHLER_OK;
 }
 
+// Segmentation host side: map_kernel over n images (one LUT per image).
+int launch_map(kohler_cuda_ctx* ctx, const MapParams& mp0, cudaStream_t stream)
+{
+    MapParams mp = mp0;
+    // unit = one warp's rows: about total / (SMs * 32 warps), 4..32 KB, never
+    // across images, so enough warps are in flight at any size
+    const long long px_per_image = (long long)mp.w * mp.h;
+    const long long target = std::min(32768ll, std::max(4096ll, px_per_image * mp.n / (ctx->sm_count * 32ll)));
+    mp.units_per_image = (int)std::max(1ll, std::min<long long>(mp.h, (px_per_image + target - 1) / target));
+    const uint32_t segs = (uint32_t)(mp.w + 15) / 16;
+    mp.seg_magic = (uint32_t)((1ull << 32) / segs + 1);
+    const long long units = (long long)mp.units_per_image * mp.n;
+    mp.flat = mp.pitch == (size_t)mp.w && mp.out_pitch == (size_t)mp.w && mp.w % 16 == 0 &&
+              ((reinterpret_cast<uintptr_t>(mp.px) | reinterpret_cast<uintptr_t>(mp.out) |
+                mp.image_stride | mp.out_stride) & 15) == 0;
+    dim3 grid((unsigned)((units + kMapWarps - 1) / kMapWarps));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kMapThreads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KC_CUDA(cudaLaunchKernelEx(&cfg, map_kernel, mp));
+    ctx->last_launches += 1;
+    return KOHLER_OK;
+}
+
+int launch_hist(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
+                size_t image_stride, uint32_t* hist, cudaStream_t stream)
+{
+    KC_CUDA(cudaMemsetAsync(hist, 0, (size_t)n * 256 * sizeof(uint32_t), stream));
+    const long long px_per_image = (long long)w * h;
+    const int bpi = (int)std::max(1ll, std::min<long long>(h, (px_per_image + 65535) / 65536));
+    const uint32_t segs = (uint32_t)(w + 15) / 16;
+    hist_kernel<<<dim3((unsigned)((long long)bpi * n)), 512, 0, stream>>>(
+        px, pitch, image_stride, w, h, bpi, (uint32_t)((1ull << 32) / segs + 1), hist);
+    KC_CUDA(cudaGetLastError());
+    ctx->last_launches += 1;
+    return KOHLER_OK;
+}
+
+// classify (mode 0) / quantize (mode 1) of one host image with a given set
+int host_classify_quantize(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                           const int* ts, int nts, uint8_t* out, int mode)
+{
+    const size_t dpitch = round_up((size_t)w, 16);
+    const size_t bytes = dpitch * (size_t)h;
+    int rc = ctx->img.ensure(std::max<size_t>(2 * bytes + 256 * 4 + (size_t)nts * 4 + 64, 64));
+    if (rc)
+        return rc;
+    uint8_t* din = static_cast<uint8_t*>(ctx->img.p);
+    uint8_t* dout = din + bytes;
+    uint32_t* dhist = reinterpret_cast<uint32_t*>(round_up(reinterpret_cast<uintptr_t>(dout + bytes), 16));
+    int* dts = reinterpret_cast<int*>(dhist + 256);
+    cudaStream_t st = ctx->stream;
+    ctx->last_launches = 0;
+    KC_CUDA(cudaMemcpy2DAsync(din, dpitch, px, pitch, (size_t)w, (size_t)h, cudaMemcpyHostToDevice, st));
+    if (nts)
+        KC_CUDA(cudaMemcpyAsync(dts, ts, (size_t)nts * 4, cudaMemcpyHostToDevice, st));
+    if (mode == 1) {
+        rc = launch_hist(ctx, din, 1, w, h, dpitch, bytes, dhist, st);
+        if (rc)
+            return rc;
+    }
+    MapParams mp{};
+    mp.px = din;
+    mp.pitch = dpitch;
+    mp.image_stride = bytes;
+    mp.out = dout;
+    mp.out_pitch = dpitch;
+    mp.out_stride = bytes;
+    mp.n = 1;
+    mp.w = w;
+    mp.h = h;
+    mp.mode = mode;
+    mp.thresholds = dts;
+    mp.ts_stride = 0;
+    mp.ts_count = nts;
+    mp.hist = dhist;
+    rc = launch_map(ctx, mp, st);
+    if (rc)
+        return rc;
+    KC_CUDA(cudaMemcpy2DAsync(out, (size_t)w, dout, dpitch, (size_t)w, (size_t)h, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaStreamSynchronize(st));
+    return KOHLER_OK;
+}
+
+// curve -> thresholds -> quantize for a device batch (K1 / K5 export the
+// pixel histograms, so the map is the only extra pass)
+int segment_device(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
+                   size_t image_stride, int k, uint8_t* out, size_t out_pitch, size_t out_stride,
+                   int* thresholds, int* ts_counts, int* status, cudaStream_t stream)
+{
+    if (n == 0)
+        return KOHLER_OK;
+    const int kk = std::max(k, 1);
+    // scratch: hist [n][256] u32, t0 / topk / counts for the mode not returned
+    const size_t hist_bytes = (size_t)n * 256 * 4;
+    const size_t scr_bytes = (size_t)n * 4 * 2 + (size_t)n * kk * 4;
+    int rc = ctx->seg.ensure(hist_bytes + scr_bytes + 64);
+    if (rc)
+        return rc;
+    uint32_t* hist = static_cast<uint32_t*>(ctx->seg.p);
+    int* scr = reinterpret_cast<int*>(hist + (size_t)n * 256);
+    BatchOut o{};
+    if (k == 0) {
+        o.t0s = thresholds;
+        o.topks = scr + 2 * (size_t)n;
+        o.topk_counts = scr;
+    } else {
+        o.t0s = scr;
+        o.topks = thresholds;
+        o.topk_counts = ts_counts;
+    }
+    o.status = status;
+    const bool tile = use_tile(n, w, h);
+    if (!tile)
+        KC_CUDA(cudaMemsetAsync(hist, 0, hist_bytes, stream));
+    rc = tile ? launch_tile(ctx, px, n, w, h, pitch, image_stride, kk, 1, o, stream, hist)
+              : launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, kk, 1, o, stream, 0, hist);
+    if (rc)
+        return rc;
+    MapParams mp{};
+    mp.px = px;
+    mp.pitch = pitch;
+    mp.image_stride = image_stride;
+    mp.out = out;
+    mp.out_pitch = out_pitch;
+    mp.out_stride = out_stride;
+    mp.n = n;
+    mp.w = w;
+    mp.h = h;
+    mp.mode = 1;
+    mp.thresholds = thresholds;
+    mp.ts_stride = kk;
+    mp.ts_counts = k == 0 ? nullptr : ts_counts;
+    mp.ts_count = 1;
+    mp.status = status;
+    mp.hist = hist;
+    mp.counts_out = k == 0 ? ts_counts : nullptr;  // 1 per frame with a boundary, else 0
+    return launch_map(ctx, mp, stream);
+}
+
 } // namespace
 
 extern "C" {
@@ -1991,6 +2407,7 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         ctx->curves.release();
         ctx->stage.release();
         ctx->hout.release();
+        ctx->seg.release();
         cudaStreamDestroy(ctx->stream);
         if (ctx->copy_stream)
             cudaStreamDestroy(ctx->copy_stream);
@@ -2109,6 +2526,102 @@ int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, in
                            static_cast<cudaStream_t>(stream));
     return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select ? 1 : 0, o,
                        static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_classify(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                         const int* thresholds, int nts, uint8_t* labels)
+{
+    if (!ctx || !px || !labels || (nts > 0 && !thresholds))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(1, w, h, pitch);
+    if (rc)
+        return rc;
+    if (nts < 0 || nts > 255)
+        return fail(KOHLER_INVALID_ARGUMENT, "classify: 0..255 thresholds");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    return host_classify_quantize(ctx, px, w, h, pitch, thresholds, nts, labels, 0);
+}
+
+int kohler_cuda_quantize(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
+                         const int* thresholds, int nts, uint8_t* out)
+{
+    if (!ctx || !px || !out || (nts > 0 && !thresholds))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(1, w, h, pitch);
+    if (rc)
+        return rc;
+    if (nts < 0 || nts > 255)
+        return fail(KOHLER_INVALID_ARGUMENT, "quantize: 0..255 thresholds");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    return host_classify_quantize(ctx, px, w, h, pitch, thresholds, nts, out, 1);
+}
+
+int kohler_cuda_segment_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w,
+                                     int h, size_t pitch, size_t image_stride, int k,
+                                     uint8_t* out, size_t out_pitch, size_t out_stride,
+                                     int* thresholds, int* ts_counts, int* status, void* stream)
+{
+    if (!ctx || (n > 0 && (!px || !out || !thresholds || !status)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(n, w, h, pitch);
+    if (rc)
+        return rc;
+    if (k < 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "segment: k must be >= 0");
+    if (out_pitch < (size_t)w || (n > 1 && (image_stride < pitch * (size_t)h ||
+                                            out_stride < out_pitch * (size_t)h)))
+        return fail(KOHLER_INVALID_ARGUMENT, "segment: bad pitch or stride");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    return segment_device(ctx, px, n, w, h, pitch, image_stride, k, out, out_pitch, out_stride,
+                          thresholds, ts_counts, status, static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_segment_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h,
+                              int k, uint8_t* out, int* thresholds, int* ts_counts, int* status)
+{
+    if (!ctx || (n > 0 && (!px || !out || !thresholds || !status)))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(n, w, h, (size_t)w);
+    if (rc)
+        return rc;
+    if (k < 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "segment: k must be >= 0");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    if (n == 0)
+        return KOHLER_OK;
+    const size_t dpitch = round_up((size_t)w, 16);
+    const size_t dstride = dpitch * (size_t)h;
+    const int kk = std::max(k, 1);
+    const size_t small = (size_t)n * (kk + 2) * 4;
+    rc = ctx->img.ensure(2 * dstride * (size_t)n + small + 64);
+    if (rc)
+        return rc;
+    uint8_t* din = static_cast<uint8_t*>(ctx->img.p);
+    uint8_t* dout = din + dstride * (size_t)n;
+    int* dts = reinterpret_cast<int*>(round_up(reinterpret_cast<uintptr_t>(dout + dstride * (size_t)n), 16));
+    int* dcnt = dts + (size_t)n * kk;
+    int* dst = dcnt + n;
+    cudaStream_t st = ctx->stream;
+    KC_CUDA(cudaMemcpy2DAsync(din, dpitch, px, (size_t)w, (size_t)w, (size_t)h * n,
+                              cudaMemcpyHostToDevice, st));
+    rc = segment_device(ctx, din, n, w, h, dpitch, dstride, k, dout, dpitch, dstride, dts, dcnt,
+                        dst, st);
+    if (rc)
+        return rc;
+    KC_CUDA(cudaMemcpy2DAsync(out, (size_t)w, dout, dpitch, (size_t)w, (size_t)h * n,
+                              cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaMemcpyAsync(thresholds, dts, (size_t)n * kk * 4, cudaMemcpyDeviceToHost, st));
+    if (ts_counts)
+        KC_CUDA(cudaMemcpyAsync(ts_counts, dcnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaMemcpyAsync(status, dst, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaStreamSynchronize(st));
+    return KOHLER_OK;
 }
 
 int kohler_cuda_band_curve_device(kohler_cuda_ctx* ctx, const uint8_t* band, int w, size_t pitch,

@@ -43,7 +43,9 @@ def test_dropin_exports_reference_api():
                 "kohler::optimal_threshold(kohler::MeanContrastCurve const&)",
                 "kohler::top_k_local_maxima(kohler::MeanContrastCurve const&, int)",
                 "kohler::merge_accumulators(std::span<kohler::ContrastCurve const, 18446744073709551615ul>)",
-                "kohler::pair_contribution(unsigned char, unsigned char, kohler::ContrastCurve&)"]:
+                "kohler::pair_contribution(unsigned char, unsigned char, kohler::ContrastCurve&)",
+                "kohler::classify(kohler::GrayImage const&, kohler::ThresholdSet const&)",
+                "kohler::quantize(kohler::GrayImage const&, kohler::ThresholdSet const&)"]:
         assert sig in out, sig
 
 
@@ -53,8 +55,10 @@ def test_kernels_are_sm100a():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True,
                           text=True).stdout
-    assert "ATOMS.POPC.INC.32" in sass      # conflict-free striped smem histograms
-    assert "VIMNMX.U16x2" in sass           # packed 16-bit max of pair values
+    assert "ATOMS.POPC.INC.32" in sass      # conflict-free striped pair (midpoint) events
+    assert "ATOMS.ADD" in sass              # packed pixel-keyed count / sign-sum words
+    assert "VIADDMNMX.S16x2.RELU" in sass   # the per-pair sign step, two pairs per instruction
+    assert "LDGSTS" in sass                 # cp.async row ring of the column walks
 
 
 def test_no_gpu_fails_loudly():

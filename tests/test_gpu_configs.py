@@ -144,7 +144,7 @@ def test_host_api_chunked_ragged_and_degenerate(ctx, ref, hw):
 
 def test_host_api_chunked_batch_vs_reference(ctx, ref):
     """Host API on 24 C3 frames: image-range chunks, each its own launch."""
-    x = synth.generate("C3", device="cpu")[:24].numpy()
+    x = synth.generate("C3", device="cuda")[:24].cpu().numpy()
     r = host_result(ctx.analyze_batch(x, K))
     exp = ref.analyze_batch(x, K, workers=1)
     check_against_reference(r, exp)

@@ -16,6 +16,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--segment", type=int, default=-1,
+                help=">= 0: time the segmentation pipeline instead (0: curve -> {t0} -> "
+                     "two-class quantize per image, bench.cpp:266-281; k: top-k quantize)")
 a = ap.parse_args()
 x = synth.generate(a.config, device="cuda")
 n, h, w = x.shape
@@ -34,8 +37,19 @@ out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
        "topk": torch.zeros((n, k), dtype=torch.int32, device="cuda"),
        "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda"),
        "status": torch.zeros(n, dtype=torch.int32, device="cuda")}
+if a.segment >= 0:
+    kk = max(a.segment, 1)
+    seg_out = torch.empty((n, h, w), dtype=torch.uint8, device="cuda")
+    seg_ts = torch.zeros((n, kk), dtype=torch.int32, device="cuda")
+
+    def call(i):
+        ctx.segment_batch_device(x[i % copies], w, h, w, w * h, n, a.segment, seg_out, w, w * h,
+                                 seg_ts, out["topk_count"], out["status"])
+else:
+    def call(i):
+        ctx.analyze_batch_device(x[i % copies], w, h, w, w * h, n, k, out)
 for i in range(a.reps):
-    ctx.analyze_batch_device(x[i % copies], w, h, w, w * h, n, k, out)
+    call(i)
 torch.cuda.synchronize()
 if a.time:
     steps = max(3, int(2e9 // max(x[0].numel(), 1)))
@@ -43,12 +57,13 @@ if a.time:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(steps):
-        ctx.analyze_batch_device(x[i % copies], w, h, w, w * h, n, k, out)
+        call(i)
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
     px = n * h * w
-    print(json.dumps({"config": a.config, "n": n, "w": w, "h": h, "ms_per_step": ms,
+    print(json.dumps({"config": a.config, "segment": a.segment, "n": n, "w": w, "h": h,
+                      "ms_per_step": ms,
                       "gpix_per_s": px / ms / 1e6, "hbm_frac": px / ms / 1e6 / 6452.8,
                       "images_per_s": n / ms * 1e3, "copies": copies, "steps": steps}))
 else:
