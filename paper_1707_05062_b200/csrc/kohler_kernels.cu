@@ -2044,13 +2044,15 @@ bool use_tile(int n, int w, int h) { return n >= 2 && (long long)w * h <= 65536;
 
 // Stage a host batch into the device, run, copy results back.
 //
-// The upload is split into up to kMaxChunks chunks on the context's copy
-// stream, each followed (on the compute stream, after an event) by the
-// launch that consumes it, so the kernels overlap the remaining PCIe
-// transfer: a single large image is cut into row bands (each band's launch
-// accumulates into the image's shared accumulator; only the last one takes
-// the tickets and finishes the curve), a batch into contiguous image ranges.
-// Small results come back in ONE device-to-host copy.
+// The upload goes in two chunks on the context's copy stream, each followed
+// (on the compute stream, after an event) by the launch that consumes it:
+// the first ~90 % of the bytes, whose accumulation (~1 B/ns on the device)
+// hides under the PCIe transfer (~0.05 B/ns) of the last ~10 %, then that
+// tail.  Each extra DMA costs ~4 us of gap, so more chunks only lose.  A
+// single large image is cut into two row bands (each launch accumulates into
+// the image's accumulator; only the last one finishes the curve), a batch
+// into two contiguous image ranges.  Small results come back in ONE
+// device-to-host copy.
 int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
                size_t image_stride, int k, int select, const BatchOut& host)
 {
@@ -2119,14 +2121,14 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     };
     const bool tile = use_tile(n, w, h);
     const size_t total = (size_t)w * h * n;
-    int chunks = (int)std::min<size_t>(kMaxChunks, std::max<size_t>(1, total / (2u << 20)));
-    if (n > 1)
-        chunks = std::min(chunks, n);
-    if (n == 1 && chunks > h)
-        chunks = h;
+    // split point (rows of the image, or images of the batch): 9/10
+    const int units = n == 1 ? h : n;
+    const int cut = total >= (4u << 20) && units >= 2 ? std::max(1, (int)((long long)units * 9 / 10)) : units;
+    const int chunks = cut < units ? 2 : 1;
+    const int bound[3] = {0, cut, units};
     for (int c = 0; c < chunks; ++c) {
         if (n == 1) {
-            const int a = (int)((long long)h * c / chunks), e = (int)((long long)h * (c + 1) / chunks);
+            const int a = bound[c], e = bound[c + 1];
             rc = upload(0, 1, a, std::min(e + 1, h));  // + the band's halo row
             if (rc)
                 return rc;
@@ -2135,7 +2137,7 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
             rc = launch_wide(ctx, dimg + (size_t)a * dpitch, 1, w, e - a, h, a, dpitch, dstride, k,
                              select, d, st, c + 1 < chunks ? 1 : 0);
         } else {
-            const int i0 = (int)((long long)n * c / chunks), i1 = (int)((long long)n * (c + 1) / chunks);
+            const int i0 = bound[c], i1 = bound[c + 1];
             rc = upload(i0, i1, 0, h);
             if (rc)
                 return rc;
