@@ -396,15 +396,21 @@ def measure_e2e(ctx, img, args):
                                        tk.ctypes.data, cnt.ctypes.data)
     for _ in range(3):
         call()
+    per = []
     st = time.perf_counter()
     for _ in range(n):
+        c0 = time.perf_counter()
         rc = call()
+        per.append(time.perf_counter() - c0)
         if rc not in (0, 1):
             raise RuntimeError("e2e call failed")
     el = time.perf_counter() - st
+    per.sort()
     d2h = 256 * 8 * 2 + 256 * 8 + 256 + 4 * 3 + 4 * K_TOP
     return {"value": w * h * n / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": w * h,
             "d2h_bytes_per_step": d2h, "steps": n,
+            "call_us": {"mean": el / n * 1e6, "median": per[n // 2] * 1e6, "min": per[0] * 1e6,
+                        "max": per[-1] * 1e6},
             "path": "kohler_cuda_analyze (host API), pinned input, wall clock"}
 
 

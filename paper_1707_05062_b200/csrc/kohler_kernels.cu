@@ -32,7 +32,6 @@ using namespace kohler_dev;
 
 namespace {
 
-constexpr int kWideThreads = 1024;
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
 constexpr int kMaxSelectLevels = 4096;
 
@@ -99,7 +98,12 @@ constexpr uint32_t kSmWacc = kSmRing + kRingBytes;   // u64 [2 copies][2 fields]
 constexpr uint32_t kSmHsTot = kSmWacc + 8192;        // u64[512]
 constexpr uint32_t kSmCorrTot = kSmHsTot + 4096;     // int[256]
 constexpr uint32_t kSmCorr = kSmCorrTot + 1024;      // int[256] border terms (corr)
-constexpr uint32_t kSmMiscEnd = kSmCorr + 1024;
+// border rows of the CTA's first image (first own row, last own row, halo):
+// the CTA's column slice, prefetched as 4-byte words at kernel start
+constexpr int kBorderPx = 1024;                        // widest prefetched slice
+constexpr uint32_t kBorderRow = kBorderPx + 16;        // words of a slice + slack
+constexpr uint32_t kSmBorder = kSmCorr + 1024;         // u8 [3][kBorderRow]
+constexpr uint32_t kSmMiscEnd = kSmBorder + 3 * kBorderRow;
 constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
 constexpr uint32_t kSmCurve = kSmVal + 4096;         // u64 sum[256], card[256]
 constexpr uint32_t kSmMean = kSmCurve + 4096;        // f64[256]
@@ -253,18 +257,103 @@ __device__ __forceinline__ void spill_w(unsigned char* sm, unsigned char* hist, 
         const uint4 v = row[(j + tid) & 7];
         h += (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
         b += (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
-        row[(j + tid) & 7] = make_uint4(0, 0, 0, 0);
+        if (clear)
+            row[(j + tid) & 7] = make_uint4(0, 0, 0, 0);
     }
     unsigned long long* wacc = reinterpret_cast<unsigned long long*>(sm + kSmWacc);
     wacc[copy * 512 + key] += h;        // hist field
     wacc[copy * 512 + 256 + key] += b;  // B field
 }
 
+// Border terms of an image band, split by columns over the CTAs that cover
+// the image (balanced: no CTA re-reads whole border rows), added straight
+// into the CTA's u64 totals after the striped counters are reduced:
+//   band first row      : corr +1 per pixel (up pair missing or not owned)
+//   last image row      : corr -1 per pixel (its down pairs were emitted as
+//                         equal fakes: the down row was the row itself)
+//   halo row (band end) : per halo pixel d under c, its owned up pair as a W
+//                         event B = 4 + sign(c - d), corr +3
+// (The halo pixels' W counts thus enter hist(); hist_out is only requested
+// for whole images, which have no halo.)
+struct BorderSlice {
+    int xa, xb;  // columns of this CTA's share
+    int wa;      // first 4-byte word of the prefetched slice (pre != null)
+};
+
+__device__ __forceinline__ BorderSlice border_slice(const WideParams& p, int img)
+{
+    // the CTAs covering the image: the whole grid for one image (no divisions)
+    uint32_t cnt = gridDim.x, idx = blockIdx.x;
+    if (p.n > 1) {
+        const long long c0 = cta_of_unit((long long)img * p.upi, p.cta_q, p.cta_r);
+        const long long c1 = cta_of_unit((long long)(img + 1) * p.upi - 1, p.cta_q, p.cta_r);
+        cnt = (uint32_t)(c1 - c0 + 1);
+        idx = (uint32_t)((long long)blockIdx.x - c0);
+    }
+    BorderSlice s;
+    if (p.w < (1 << 22)) {  // 32-bit products (cnt <= 1024)
+        s.xa = (int)((uint32_t)p.w * idx / cnt);
+        s.xb = (int)((uint32_t)p.w * (idx + 1) / cnt);
+    } else {
+        s.xa = (int)((long long)p.w * idx / cnt);
+        s.xb = (int)((long long)p.w * (idx + 1) / cnt);
+    }
+    s.wa = s.xa >> 2;
+    return s;
+}
+
+// Issue the cp.async word copies of the slice's border rows (rows are
+// 16-byte aligned: K1 inputs are staged otherwise; the words stay inside the
+// pitch).  One commit group, older than the ring's first rows.
+__device__ __forceinline__ void border_prefetch(const WideParams& p, int img, const BorderSlice& s,
+                                                uint32_t dst)
+{
+    const uint8_t* base = p.px + (size_t)img * p.image_stride;
+    const int ylast = p.band_rows - 1;
+    const bool halo = p.r0 + ylast != p.h_total - 1;
+    const int nw = ((s.xb + 3) >> 2) - s.wa;
+    for (int i = threadIdx.x; i < 3 * nw; i += kWalkThreads) {
+        const int r = i / nw, wi = i - r * nw;
+        if (r == 2 && !halo)
+            break;
+        const int y = r == 0 ? 0 : ylast + (r - 1);
+        const uint8_t* src = base + (size_t)y * p.pitch + 4 * (s.wa + wi);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + r * kBorderRow + 4 * wi),
+                     "l"(src)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void border_pass(const WideParams& p, int img, const BorderSlice& s,
+                                            const uint8_t* pre, unsigned long long* wacc,
+                                            int* corr_tot)
+{
+    const uint8_t* base = p.px + (size_t)img * p.image_stride;
+    const int ylast = p.band_rows - 1;
+    const bool img_last = p.r0 + ylast == p.h_total - 1;
+    const uint8_t* rl = base + (size_t)ylast * p.pitch;
+    for (int x = s.xa + (int)threadIdx.x; x < s.xb; x += kWalkThreads) {
+        const int o = x - 4 * s.wa;
+        const int v0 = pre ? pre[o] : base[x];
+        const int c = pre ? pre[kBorderRow + o] : rl[x];
+        atomicAdd(&corr_tot[v0], 1);
+        if (img_last) {
+            atomicAdd(&corr_tot[c], -1);
+        } else {
+            const int d = pre ? pre[2 * kBorderRow + o] : rl[p.pitch + x];
+            atomicAdd(&wacc[d], 1ull);
+            atomicAdd(&wacc[256 + d], (unsigned long long)(4 + (c > d) - (c < d)));
+            atomicAdd(&corr_tot[d], 3);
+        }
+    }
+}
+
 // CTA flush of one image's partial: reduce the striped counters (clearing
 // them for the next image), form the 512 combinations, REDG them into the
 // image's accumulator (finish_kernel takes it from there).
 __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, unsigned char* hist,
-                            bool clear)
+                            bool clear, bool two_w, bool prefetched)
 {
     using namespace kohler_walk;
     const int tid = threadIdx.x;
@@ -278,16 +367,20 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
         for (int j = 0; j < 8; ++j) {
             const uint4 v = row[(j + t) & 7];
             s += (unsigned long long)v.x + v.y + v.z + v.w;
-            row[(j + t) & 7] = make_uint4(0, 0, 0, 0);
+            if (clear)  // the CTA's last image: nothing reads the counters again
+                row[(j + t) & 7] = make_uint4(0, 0, 0, 0);
         }
         hs_tot[t] = s;
-        spill_w(sm, hist, t, clear);
+        if (two_w || t < 256)
+            spill_w(sm, hist, t, clear);
         if (t < 256) {
             int* cr = reinterpret_cast<int*>(sm + kSmCorr);
             corr_tot[t] = cr[t];
             cr[t] = 0;
         }
     }
+    __syncthreads();
+    border_pass(p, img, border_slice(p, img), prefetched ? sm + kSmBorder : nullptr, wacc, corr_tot);
     __syncthreads();
     // the accumulators may still be read / reset by the previous finish_kernel
     pdl_wait();
@@ -318,99 +411,12 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
                 atomicAdd(p.hist_out + (size_t)img * 256 + t, hv);
         }
     }
-    __syncthreads();
-    for (int t = tid; t < 1024; t += kWalkThreads)
-        wacc[t] = 0;
+    if (clear) {
+        __syncthreads();
+        for (int t = tid; t < 1024; t += kWalkThreads)
+            wacc[t] = 0;
+    }
     phase(3);
-}
-
-// A lane's 16-pixel segment: unit u covers flattened (row, segment) indices
-// [32u, 32u + 32) of an image band; lane L takes 32u + L.  Cursor walks a
-// warp's contiguous unit range without divisions.
-struct Cursor {
-    int y;    // band-relative row
-    int seg;  // segment in the row
-    // advance by one unit = 32 segments = adv_q rows + adv_r segments
-    __device__ __forceinline__ void advance(int nseg, int adv_q, int adv_r)
-    {
-        seg += adv_r;
-        y += adv_q;
-        if (seg >= nseg) {
-            seg -= nseg;
-            ++y;
-        }
-    }
-};
-
-struct Segment {
-    uint32_t c[4];
-    uint32_t n[4];
-    uint32_t rn;
-};
-
-// Geometry both accumulation kernels need per segment.
-struct Geo {
-    size_t pitch;
-    int w;
-    int band_rows;  // own rows
-    int r0;         // global row of buffer row 0
-    int h_total;    // global image height
-};
-
-// Loads of one lane's segment at band-relative (y, seg): the row, the row
-// below (when the pair exists) and the right-neighbour byte (when inside the
-// row).  No shuffles: every load is issued a unit ahead of its use.
-template <bool VEC>
-__device__ __forceinline__ void fetch(const Geo& p, const uint8_t* base, int y, int seg,
-                                      Segment& s)
-{
-    const int x0 = seg << 4;
-    const uint8_t* row = base + (size_t)y * p.pitch;
-    if (y < p.band_rows) {
-        load_segment<VEC>(row, x0, p.w, s.c);
-        if (p.r0 + y + 1 < p.h_total)
-            load_segment<VEC>(row + p.pitch, x0, p.w, s.n);
-        if (x0 + 16 < p.w)
-            s.rn = __ldg(row + x0 + 16);
-    }
-}
-
-// Accumulate one lane's segment.
-// ALIGNED (w % 16 == 0): row starts / row ends are fixed inline with
-// predicated, conflict-free corr updates (a row-end segment has no garbage
-// bytes: its right neighbour becomes its own last pixel, corr -1; a row start
-// has no left pair, corr +1), so only lanes in the band's first row, the
-// image's last row or the halo row take the divergent border_terms path.
-// General widths: every non-interior lane takes border_terms.
-template <bool ALIGNED, class CorrAdd>
-__device__ __forceinline__ void process(const Geo& p, unsigned char* sm, int y, int seg,
-                                        uint32_t lane4, Segment& s, const CorrAdd& corr)
-{
-    const int x0 = seg << 4;
-    const bool active = y < p.band_rows;
-    const bool rows_ok = y != 0 && y + 1 < p.band_rows;
-    const bool inner = ALIGNED ? (active && rows_ok)
-                               : (active && rows_ok && x0 != 0 && x0 + 16 < p.w);
-    if (!__all_sync(0xFFFFFFFFu, inner)) {
-        if (!active)
-            return;
-        if (!inner && (!ALIGNED || !rows_ok)) {
-            const int gy = p.r0 + y;
-            StepGeom geom{p.w, y, p.band_rows, gy, p.h_total, x0};
-            border_terms(corr, geom, s.c, s.n, s.rn, gy + 1 < p.h_total);
-            accumulate_segment(sm, s.c, s.n, s.rn, lane4);
-            return;
-        }
-    }
-    if (ALIGNED) {
-        if (x0 == 0)
-            corr(s.c[0] & 0xFFu, 1);
-        if (x0 + 16 >= p.w) {
-            s.rn = s.c[3] >> 24;
-            corr(s.rn, -1);
-        }
-    }
-    accumulate_segment(sm, s.c, s.n, s.rn, lane4);
 }
 
 // ---------------------------------------------------------------------------
@@ -511,61 +517,6 @@ __device__ __forceinline__ GroupFlags group_flags(const LaneGeo& L, bool aligned
     return f;
 }
 
-// Border rows of a group (rare: the band's first row, the band's last row),
-// done once per group after its walk from a re-read of the rows involved:
-//   band first row      : corr +1 per pixel (up pair missing or not owned)
-//   last image row      : corr -1 per pixel (its down pairs were emitted as
-//                         equal fakes: the down row was the row itself)
-//   halo row (band end) : per halo pixel d under c, its owned up pair as a W
-//                         event B = 4 + sign(c - d) = 5 - q(c -> d), corr +3
-template <bool ALIGNED>
-__device__ __noinline__ void border_rows(const WideParams& p, uint32_t smbase, const LaneGeo& G,
-                                         int r0, int r1, uint32_t lane4)
-{
-    using namespace kohler_walk;
-    // this lane walked rows y0 + [r0, r1) of its column (clipped to its own rows)
-    r1 = min(r1, G.nrows);
-    if (r0 >= r1)
-        return;
-    const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
-    auto load16 = [&](int y, uint32_t (&w)[4]) {
-        const uint8_t* rp = G.p + (size_t)(y - G.y0 + 1) * p.pitch;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                word |= (4 * jj + b < nreal ? (uint32_t)rp[4 * jj + b] : 0u) << (8 * b);
-            w[jj] = word;
-        }
-    };
-    auto byte = [](const uint32_t (&w)[4], int i) { return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu; };
-    if (G.y0 + r0 == 0) {
-        uint32_t w[4];
-        load16(0, w);
-        for (int i = 0; i < nreal; ++i)
-            red_add(smbase + kSmCorr + (byte(w, i) << 2), 1u);
-    }
-    const int ylast = G.y0 + r1 - 1;
-    if (ylast == p.band_rows - 1) {
-        uint32_t c[4];
-        load16(ylast, c);
-        if (p.r0 + ylast == p.h_total - 1) {
-            for (int i = 0; i < nreal; ++i)
-                red_add(smbase + kSmCorr + (byte(c, i) << 2), 0xFFFFFFFFu);
-        } else {
-            uint32_t d[4];
-            load16(ylast + 1, d);
-            for (int i = 0; i < nreal; ++i) {
-                const uint32_t cv = byte(c, i), dv = byte(d, i);
-                const uint32_t b = 4u + (cv > dv) - (cv < dv);  // 4 + sign(c - d)
-                red_add(kHistAbs + kOffW0 + (dv << 8) + lane4, (b << 16) | 1u);
-                red_add(smbase + kSmCorr + (dv << 2), 3u);
-            }
-        }
-    }
-}
-
 // A warp walks the contiguous run [ua, ub) of "units" of one image: unit u =
 // row u % R of the 32 column walks of group u / R.  The run is a sequence of
 // segments (one per group touched); a segment of L rows is L + 2 ring
@@ -573,7 +524,29 @@ __device__ __noinline__ void border_rows(const WideParams& p, uint32_t smbase, c
 // one position per row.  Rows stream through the warp's 4-slot shared ring,
 // prefetched 3 positions ahead across segment boundaries.  The W copy
 // alternates with the position parity (bounds each copy's events).
-template <bool ALIGNED>
+// Clear the counter block (one W copy: rows 256..511 only have their Hs half
+// in use) and the per-CTA scratch.
+template <bool TWO_W>
+__device__ __forceinline__ void zero_counters(unsigned char* sm, unsigned char* hist)
+{
+    using namespace kohler_walk;
+    uint4* z = reinterpret_cast<uint4*>(hist);
+    constexpr int kFull = TWO_W ? (int)(kHistBytes / 16) : (int)(kHistBytes / 32);
+    for (int i = threadIdx.x; i < kFull; i += kWalkThreads)
+        z[i] = make_uint4(0, 0, 0, 0);
+    if (!TWO_W) {
+        // rows 256..511, bytes [0, 128) of each: 8 uint4 per row
+        for (int i = threadIdx.x; i < 256 * 8; i += kWalkThreads)
+            z[kFull + (i >> 3) * 16 + (i & 7)] = make_uint4(0, 0, 0, 0);
+    }
+    uint4* zw = reinterpret_cast<uint4*>(sm + kSmWacc);
+    for (int i = threadIdx.x; i < 8192 / 16; i += kWalkThreads)
+        zw[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 256)
+        reinterpret_cast<int*>(sm + kSmCorr)[threadIdx.x] = 0;
+}
+
+template <bool ALIGNED, bool TWO_W>
 __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
                                            unsigned char* hist, uint32_t smbase,
                                            const uint8_t* base, long long ua, long long ub,
@@ -610,14 +583,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     }
     if (zero_first) {
         // clear the counters while the first rows are in flight
-        uint4* z = reinterpret_cast<uint4*>(hist);
-        for (int i = threadIdx.x; i < (int)(kHistBytes / 16); i += kWalkThreads)
-            z[i] = make_uint4(0, 0, 0, 0);
-        uint4* zw = reinterpret_cast<uint4*>(sm + kSmWacc);
-        for (int i = threadIdx.x; i < 8192 / 16; i += kWalkThreads)
-            zw[i] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x < 256)
-            reinterpret_cast<int*>(sm + kSmCorr)[threadIdx.x] = 0;
+        zero_counters<TWO_W>(sm, hist);
         __syncthreads();
         phase(1);
     }
@@ -647,7 +613,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             constexpr int KIND = decltype(kind)::value;  // 0 absorb, 1 prime, 2 process
             constexpr bool CROSS = decltype(cross)::value;  // prefetch may cross into the next segment
             constexpr int WC = decltype(wc)::value;
-            constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
+            constexpr uint32_t kOffW = (WC && TWO_W) ? kOffW1 : kOffW0;
             const uint32_t q = pos + (uint32_t)j;
             // slot q & 3 was committed 3 groups ago; <= 2 younger groups may pend
             asm volatile("cp.async.wait_group 2;" ::: "memory");
@@ -740,11 +706,6 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         }
         if (j < P)
             step(X, Y, j, K2{}, W0{}, CR{});
-        const bool border = __any_sync(0xFFFFFFFFu, G.nrows > 0 && r0 < min(r1, G.nrows) &&
-                                                          ((G.y0 + r0 == 0) ||
-                                                           (G.y0 + min(r1, G.nrows) == p.band_rows)));
-        if (border)
-            border_rows<ALIGNED>(p, smbase, G, r0, r1, lane4);
         if (!has_next)
             break;
         pos += (uint32_t)P;
@@ -756,7 +717,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <bool ALIGNED>
+template <bool ALIGNED, bool TWO_W>
 __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -779,6 +740,11 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
             i_first = (int)(cs / p.upi);
             i_last = (int)((ce - 1) / p.upi);
         }
+        // the first image's border slice arrives with the first ring rows
+        const BorderSlice bs = border_slice(p, i_first);
+        const bool prefetched = bs.xb - bs.xa <= kBorderPx;
+        if (prefetched)
+            border_prefetch(p, i_first, bs, smbase + kSmBorder);
         for (int img = i_first; img <= i_last; ++img) {
             const long long ibase = (long long)img * p.upi;
             const long long a = (cs > ibase ? cs : ibase) - ibase;
@@ -789,12 +755,12 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
                 const long long n = eb - ea;
                 const long long wa = ea + n * warp / kWalkWarps;
                 const long long wb = ea + n * (warp + 1) / kWalkWarps;
-                walk_range<ALIGNED>(p, sm, hist, smbase, base, wa, wb, !zeroed);
+                walk_range<ALIGNED, TWO_W>(p, sm, hist, smbase, base, wa, wb, !zeroed);
                 warp_end();
                 zeroed = true;
                 __syncthreads();
                 if (eb < b) {
-                    for (int t = tid; t < 512; t += kWalkThreads)
+                    for (int t = tid; t < (TWO_W ? 512 : 256); t += kWalkThreads)
                         spill_w(sm, hist, t);
                     __syncthreads();
                 }
@@ -803,7 +769,9 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
                 phase(2);
                 pdl_trigger();  // the next launch may start as SMs free up
             }
-            flush_image(p, img, sm, hist, img < i_last);  // the last image: no re-zeroing
+            asm volatile("cp.async.wait_group 0;" ::: "memory");  // border words (walk-less threads)
+            flush_image(p, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first);
+            // (the last image: no re-zeroing)
             flushed = true;
         }
     }
@@ -1736,6 +1704,11 @@ cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, 
 }
 
 // Launch K1 over n images whose buffers hold band_rows own rows (+ halo).
+#ifndef KOHLER_SINGLE_W
+#define KOHLER_SINGLE_W 0
+#endif
+constexpr bool kSingleW = KOHLER_SINGLE_W != 0;
+
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
                 const BatchOut& o, cudaStream_t stream, int no_finish = 0,
@@ -1800,9 +1773,20 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     // the warps in contiguous runs of k_w segments (k_w <= units_w / R + 2):
     // copy 0 takes ceil(L/2) rows per segment plus <= 1 halo row per
     // segment, 16 pixels each: <= 16 (E/2 + 1.5 (E/R + 2 W)) <= kMaxEvents.
+    // One W copy (all positions, plus the halo rows): <= 16 (E + E/R + 2 W);
+    // used when every CTA's range fits one such epoch (no spill at all), which
+    // saves a quarter of the counter block's zeroing and flushing.
+    bool two_w;
     {
-        const double cap = (double)kohler_walk::kMaxEventsPerWord / 16.0 - 3.0 * kWalkWarps;
-        p.epoch = (int)std::max(1.0, std::floor(cap / (0.5 + 1.5 / (double)R)));
+        const double cap2 = (double)kohler_walk::kMaxEventsPerWord / 16.0 - 3.0 * kWalkWarps;
+        const double cap1 = (double)kohler_walk::kMaxEventsPerWord / 16.0 - 2.0 * kWalkWarps;
+        const long long e1 = (long long)std::max(1.0, std::floor(cap1 / (1.0 + 1.0 / (double)R)));
+        const long long range = U / G + (U % G ? 1 : 0);
+        // measured (r01 phase probe): one copy shortens zeroing / flushing by
+        // 0.5 us but back-to-back same-word atomics slow the walk as much, so
+        // two copies stay the default; one copy remains for ablation
+        two_w = !kSingleW || range > e1;
+        p.epoch = two_w ? (int)std::max(1.0, std::floor(cap2 / (0.5 + 1.5 / (double)R))) : (int)e1;
     }
     p.acc = static_cast<unsigned long long*>(ctx->acc.p);
     p.copies = copies;
@@ -1849,9 +1833,13 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     }
     // the smem opt-in is per device; remember it per context
     if (!ctx->wide_attr_set) {
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         ctx->wide_attr_set = true;
     }
@@ -1867,9 +1855,11 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (w % 16 == 0)
-        KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<true>, p));
+        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true>, p)
+                      : cudaLaunchKernelEx(&cfg, walk_kernel<true, false>, p));
     else
-        KC_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<false>, p));
+        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<false, true>, p)
+                      : cudaLaunchKernelEx(&cfg, walk_kernel<false, false>, p));
     ctx->last_launches += 1;
     if (!no_finish) {
         FinishParams fp{};
