@@ -101,7 +101,7 @@ constexpr uint32_t kSmCorr = kSmCorrTot + 1024;      // int[256] border terms (c
 // border rows of the CTA's first image (first own row, last own row, halo):
 // the CTA's column slice, prefetched as 4-byte words at kernel start
 constexpr int kBorderPx = 1024;                        // widest prefetched slice
-constexpr uint32_t kBorderRow = kBorderPx + 16;        // words of a slice + slack
+constexpr uint32_t kBorderRow = kBorderPx + 32;        // 16-byte chunks of a slice + slack
 constexpr uint32_t kSmBorder = kSmCorr + 1024;         // u8 [3][kBorderRow]
 constexpr uint32_t kSmMiscEnd = kSmBorder + 3 * kBorderRow;
 constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
@@ -277,7 +277,7 @@ __device__ __forceinline__ void spill_w(unsigned char* sm, unsigned char* hist, 
 // for whole images, which have no halo.)
 struct BorderSlice {
     int xa, xb;  // columns of this CTA's share
-    int wa;      // first 4-byte word of the prefetched slice (pre != null)
+    int ca;      // first 16-byte chunk of the prefetched slice (pre != null)
 };
 
 __device__ __forceinline__ BorderSlice border_slice(const WideParams& p, int img)
@@ -298,29 +298,31 @@ __device__ __forceinline__ BorderSlice border_slice(const WideParams& p, int img
         s.xa = (int)((long long)p.w * idx / cnt);
         s.xb = (int)((long long)p.w * (idx + 1) / cnt);
     }
-    s.wa = s.xa >> 2;
+    s.ca = s.xa >> 4;
     return s;
 }
 
-// Issue the cp.async word copies of the slice's border rows (rows are
-// 16-byte aligned: K1 inputs are staged otherwise; the words stay inside the
-// pitch).  One commit group, older than the ring's first rows.
+// Issue the cp.async copies of the slice's border rows in 16-byte chunks
+// (rows are 16-byte aligned: K1 inputs are staged otherwise; a chunk stays
+// inside the pitch).  One commit group.
 __device__ __forceinline__ void border_prefetch(const WideParams& p, int img, const BorderSlice& s,
                                                 uint32_t dst)
 {
     const uint8_t* base = p.px + (size_t)img * p.image_stride;
     const int ylast = p.band_rows - 1;
-    const bool halo = p.r0 + ylast != p.h_total - 1;
-    const int nw = ((s.xb + 3) >> 2) - s.wa;
-    for (int i = threadIdx.x; i < 3 * nw; i += kWalkThreads) {
-        const int r = i / nw, wi = i - r * nw;
-        if (r == 2 && !halo)
-            break;
+    const int rows = p.r0 + ylast != p.h_total - 1 ? 3 : 2;  // + the halo row
+    const int nc = ((s.xb + 15) >> 4) - s.ca;
+    for (int i = threadIdx.x; i < rows * nc; i += kWalkThreads) {
+        const int r = i >= nc ? (i >= 2 * nc ? 2 : 1) : 0, ci = i - r * nc;
         const int y = r == 0 ? 0 : ylast + (r - 1);
-        const uint8_t* src = base + (size_t)y * p.pitch + 4 * (s.wa + wi);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + r * kBorderRow + 4 * wi),
+        const uint8_t* src = base + (size_t)y * p.pitch + 16 * (s.ca + ci);
+#ifndef KOHLER_PROBE_NO_BORDER_COPY
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + r * kBorderRow + 16 * ci),
                      "l"(src)
                      : "memory");
+#else
+        asm volatile("" ::"r"(dst + r * kBorderRow + 16 * ci), "l"(src));
+#endif
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -334,7 +336,7 @@ __device__ __forceinline__ void border_pass(const WideParams& p, int img, const 
     const bool img_last = p.r0 + ylast == p.h_total - 1;
     const uint8_t* rl = base + (size_t)ylast * p.pitch;
     for (int x = s.xa + (int)threadIdx.x; x < s.xb; x += kWalkThreads) {
-        const int o = x - 4 * s.wa;
+        const int o = x - 16 * s.ca;
         const int v0 = pre ? pre[o] : base[x];
         const int c = pre ? pre[kBorderRow + o] : rl[x];
         atomicAdd(&corr_tot[v0], 1);
@@ -583,7 +585,9 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     }
     if (zero_first) {
         // clear the counters while the first rows are in flight
+        phase(4);
         zero_counters<TWO_W>(sm, hist);
+        phase(5);
         __syncthreads();
         phase(1);
     }
@@ -728,6 +732,11 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     phase(0);
+    // Touch every 64-byte line of the parameter block at once: a launch's
+    // parameters are cold in the constant cache, and the prologue's branches
+    // on them would otherwise serialise one miss per line.
+    asm volatile("" ::"l"(p.px), "r"(p.band_rows), "l"(p.T), "r"(p.epoch), "l"(p.cta_q),
+                 "l"(p.acc), "l"(p.hist_out), "l"(p.t0s), "l"(p.status));
     const long long rb = blockIdx.x;
     const long long cs = rb * p.cta_q + (rb < p.cta_r ? rb : p.cta_r);
     const long long ce = cs + p.cta_q + (rb < p.cta_r ? 1 : 0);

@@ -43,6 +43,31 @@ int main(int argc, char** argv)
     cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     printf("pipelined (PDL) back-to-back: %.2f us/step\n", ms * 1000 / 200);
+    {
+        // phases of the last pipelined launch (warm instruction / constant caches)
+        static unsigned long long pp[2048][8];
+        cudaMemcpyFromSymbol(pp, g_phase, sizeof(pp));
+        const int G = ctx->last_grid;
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < G; ++c) t0 = std::min(t0, pp[c][0]);
+        double pro = 0, zl = 0, sy = 0, mn = 0, fl = 0, mx = 0, pk = 0;
+        for (int c = 0; c < G; ++c) {
+            pk += (pp[c][6] - pp[c][0]) / 1e3;
+            pro += (pp[c][4] - pp[c][0]) / 1e3;
+            zl += (pp[c][5] - pp[c][4]) / 1e3;
+            sy += (pp[c][1] - pp[c][5]) / 1e3;
+            mn += (pp[c][2] - pp[c][1]) / 1e3;
+            fl += (pp[c][3] - pp[c][2]) / 1e3;
+            mx = std::max(mx, (pp[c][3] - t0) / 1e3);
+        }
+        printf("raw stamp mod 1000 ns (CTA 0..5, phases 0,4,5,1): ");
+        for (int c = 0; c < 6; ++c)
+            printf("[%llu %llu %llu %llu] ", pp[c][0] % 1000, pp[c][4] % 1000, pp[c][5] % 1000, pp[c][1] % 1000);
+        printf("\n");
+        printf("pipelined: kernel setup %.2f of ", pk / G);
+        printf("pipelined last launch: prologue %.2f, zero loop %.2f, barrier %.2f, main %.2f, flush %.2f us (avg); "
+               "first start -> last flush end %.2f us\n", pro / G, zl / G, sy / G, mn / G, fl / G, mx);
+    }
     std::vector<double> tot;
     for (int r = 0; r < reps; ++r) {
         cudaStreamSynchronize(st);
@@ -70,7 +95,16 @@ int main(int argc, char** argv)
         avgMain += us(c, 2) - us(c, 1);
         mainMin = std::min(mainMin, us(c, 2)); mainMax = std::max(mainMax, us(c, 2));
         avgFlush += us(c, 3) - us(c, 2);
-        if (ph[c][4] > ph[c][0] && ph[c][4] >= ph[c][3]) lastCta = c;
+    }
+    {
+        double pro = 0, zl = 0, sy = 0;
+        for (int c = 0; c < G; ++c) {
+            pro += us(c, 4) - us(c, 0);
+            zl += us(c, 5) - us(c, 4);
+            sy += us(c, 1) - us(c, 5);
+        }
+        printf("zero phase split (thread 0): prologue %.2f, zero loop %.2f, barrier wait %.2f us\n",
+               pro / G, zl / G, sy / G);
     }
     printf("last CTA start +%.2f us; avg zero %.2f; avg main %.2f; main done min %.2f max %.2f; avg flush %.2f; total %.2f us\n",
            lastStart, avgZero / G, avgMain / G, mainMin, mainMax, avgFlush / G, (tend - t0) / 1e3);
