@@ -103,7 +103,12 @@ constexpr uint32_t kSmCorr = kSmCorrTot + 1024;      // int[256] border terms (c
 constexpr int kBorderPx = 1024;                        // widest prefetched slice
 constexpr uint32_t kBorderRow = kBorderPx + 32;        // 16-byte chunks of a slice + slack
 constexpr uint32_t kSmBorder = kSmCorr + 1024;         // u8 [3][kBorderRow]
-constexpr uint32_t kSmMiscEnd = kSmBorder + 3 * kBorderRow;
+constexpr uint32_t kSmHb = (kSmBorder + 3 * kBorderRow + 15) & ~15u;  // u32 [2][256] halo W events
+// a copy of the launch parameters for the flush: by then the constant cache
+// has lost them to the walk's instruction stream (each cold LDC cost ~0.25 us)
+constexpr uint32_t kSmParams = kSmHb + 2048;
+constexpr uint32_t kSmBslice = kSmParams + 256;  // BorderSlice of the CTA's first image
+constexpr uint32_t kSmMiscEnd = kSmBslice + 16;
 constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
 constexpr uint32_t kSmCurve = kSmVal + 4096;         // u64 sum[256], card[256]
 constexpr uint32_t kSmMean = kSmCurve + 4096;        // f64[256]
@@ -132,9 +137,13 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 #ifdef KOHLER_PHASES
 // Debug builds only (tools/phase_probe.cu): per-CTA globaltimer stamps.
-__device__ unsigned long long g_phase[2048][8];
+__device__ unsigned long long g_phase[2048][12];
 __device__ unsigned g_smid[2048];
 __device__ int g_rot;
+__device__ unsigned long long g_sm_end[2][256];  // per SM: exit stamp of the last two launches
+__device__ unsigned g_launch;
+__device__ long long g_cyc[2048][8];
+#define KCYC(i) do { if (threadIdx.x == 0 && blockIdx.x < 2048) g_cyc[blockIdx.x][i] = clock64(); } while (0)
 __device__ unsigned long long g_wend[2048][32];  // per-warp end of its last walk
 __device__ __forceinline__ void phase(int i)
 {
@@ -147,6 +156,11 @@ __device__ __forceinline__ void phase(int i)
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             g_smid[blockIdx.x] = sm;
         }
+        if (i == 7) {  // exit stamp per SM, alternating by launch parity
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_sm_end[g_launch & 1][sm & 255] = t;
+        }
     }
 }
 __device__ __forceinline__ void warp_end()
@@ -158,6 +172,7 @@ __device__ __forceinline__ void warp_end()
     }
 }
 #else
+#define KCYC(i) do { } while (0)
 __device__ __forceinline__ void phase(int) {}
 __device__ __forceinline__ void warp_end() {}
 #endif
@@ -208,6 +223,10 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishParams p)
         }
         sval[r] = (long long)s;
     }
+#ifdef KOHLER_PHASES
+    if (tid == 0 && img == 0)
+        ++g_launch;
+#endif
     __syncthreads();
     const int warp = tid >> 5;
     if (warp == 0)
@@ -328,34 +347,39 @@ __device__ __forceinline__ void border_prefetch(const WideParams& p, int img, co
 }
 
 __device__ __forceinline__ void border_pass(const WideParams& p, int img, const BorderSlice& s,
-                                            const uint8_t* pre, unsigned long long* wacc,
-                                            int* corr_tot)
+                                            const uint8_t* pre, uint32_t* hb, int* corr_tot)
 {
+    // 32-bit shared atomics only (a u64 shared atomicAdd is a CAS loop, and
+    // border values repeat: it serialised the whole pass)
     const uint8_t* base = p.px + (size_t)img * p.image_stride;
     const int ylast = p.band_rows - 1;
     const bool img_last = p.r0 + ylast == p.h_total - 1;
     const uint8_t* rl = base + (size_t)ylast * p.pitch;
+    KCYC(0);
     for (int x = s.xa + (int)threadIdx.x; x < s.xb; x += kWalkThreads) {
         const int o = x - 16 * s.ca;
         const int v0 = pre ? pre[o] : base[x];
         const int c = pre ? pre[kBorderRow + o] : rl[x];
+        KCYC(1);
         atomicAdd(&corr_tot[v0], 1);
         if (img_last) {
             atomicAdd(&corr_tot[c], -1);
         } else {
             const int d = pre ? pre[2 * kBorderRow + o] : rl[p.pitch + x];
-            atomicAdd(&wacc[d], 1ull);
-            atomicAdd(&wacc[256 + d], (unsigned long long)(4 + (c > d) - (c < d)));
+            atomicAdd(&hb[d], 1u);
+            atomicAdd(&hb[256 + d], (uint32_t)(4 + (c > d) - (c < d)));
             atomicAdd(&corr_tot[d], 3);
         }
+        KCYC(2);
     }
+    KCYC(3);
 }
 
 // CTA flush of one image's partial: reduce the striped counters (clearing
 // them for the next image), form the 512 combinations, REDG them into the
 // image's accumulator (finish_kernel takes it from there).
 __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, unsigned char* hist,
-                            bool clear, bool two_w, bool prefetched)
+                            bool clear, bool two_w, bool prefetched, bool first)
 {
     using namespace kohler_walk;
     const int tid = threadIdx.x;
@@ -382,15 +406,25 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
         }
     }
     __syncthreads();
-    border_pass(p, img, border_slice(p, img), prefetched ? sm + kSmBorder : nullptr, wacc, corr_tot);
+    phase(8);
+    uint32_t* hb = reinterpret_cast<uint32_t*>(sm + kSmHb);
+    KCYC(4);
+    // the first image's slice was computed at kernel start (gridDim / params
+    // are cold in the constant cache by now)
+    border_pass(p, img, first ? *reinterpret_cast<const BorderSlice*>(sm + kSmBslice) : border_slice(p, img),
+                prefetched ? sm + kSmBorder : nullptr, hb, corr_tot);
+    KCYC(5);
     __syncthreads();
+    KCYC(6);
+    phase(9);
     // the accumulators may still be read / reset by the previous finish_kernel
     pdl_wait();
+    phase(10);
     for (int t = tid; t < 512; t += kWalkThreads) {
-        auto hist = [&](int v) { return (long long)(wacc[v] + wacc[512 + v]); };
+        auto hist = [&](int v) { return (long long)(wacc[v] + wacc[512 + v] + hb[v]); };
         long long val;
         if (t < 256) {
-            const long long bs = (long long)(wacc[256 + t] + wacc[512 + 256 + t]);
+            const long long bs = (long long)(wacc[256 + t] + wacc[512 + 256 + t] + hb[256 + t]);
             val = bs - 4ll * hist(t);  // card first difference
         } else {
             const int u = t - 256;  // sum second difference
@@ -415,8 +449,11 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
     }
     if (clear) {
         __syncthreads();
-        for (int t = tid; t < 1024; t += kWalkThreads)
+        for (int t = tid; t < 1024; t += kWalkThreads) {
             wacc[t] = 0;
+            if (t < 512)
+                hb[t] = 0;
+        }
     }
     phase(3);
 }
@@ -546,6 +583,8 @@ __device__ __forceinline__ void zero_counters(unsigned char* sm, unsigned char* 
         zw[i] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x < 256)
         reinterpret_cast<int*>(sm + kSmCorr)[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < 512; i += kWalkThreads)
+        reinterpret_cast<uint32_t*>(sm + kSmHb)[i] = 0;
 }
 
 template <bool ALIGNED, bool TWO_W>
@@ -722,7 +761,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
 }
 
 template <bool ALIGNED, bool TWO_W>
-__global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams p)
+__global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_constant__ WideParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
     const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
@@ -730,6 +769,10 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
         __trap();  // the fixed counter address would overlap the scratch (never seen)
     unsigned char* hist = sm + (kHistAbs - smbase);
     const int tid = threadIdx.x;
+    static_assert(sizeof(WideParams) <= 256 && sizeof(WideParams) % 4 == 0, "params copy");
+    if (tid < (int)(sizeof(WideParams) / 4))  // read back after the zeroing barrier
+        reinterpret_cast<uint32_t*>(sm + kSmParams)[tid] = reinterpret_cast<const uint32_t*>(&p)[tid];
+    const WideParams& ps = *reinterpret_cast<const WideParams*>(sm + kSmParams);
     const int warp = tid >> 5;
     phase(0);
     // Touch every 64-byte line of the parameter block at once: a launch's
@@ -751,6 +794,8 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
         }
         // the first image's border slice arrives with the first ring rows
         const BorderSlice bs = border_slice(p, i_first);
+        if (tid == 0)
+            *reinterpret_cast<BorderSlice*>(sm + kSmBslice) = bs;
         const bool prefetched = bs.xb - bs.xa <= kBorderPx;
         if (prefetched)
             border_prefetch(p, i_first, bs, smbase + kSmBorder);
@@ -779,7 +824,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const WideParams 
                 pdl_trigger();  // the next launch may start as SMs free up
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");  // border words (walk-less threads)
-            flush_image(p, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first);
+            flush_image(ps, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first, img == i_first);
             // (the last image: no re-zeroing)
             flushed = true;
         }

@@ -45,7 +45,7 @@ int main(int argc, char** argv)
     printf("pipelined (PDL) back-to-back: %.2f us/step\n", ms * 1000 / 200);
     {
         // phases of the last pipelined launch (warm instruction / constant caches)
-        static unsigned long long pp[2048][8];
+        static unsigned long long pp[2048][12];
         cudaMemcpyFromSymbol(pp, g_phase, sizeof(pp));
         const int G = ctx->last_grid;
         unsigned long long t0 = ~0ull;
@@ -64,6 +64,38 @@ int main(int argc, char** argv)
         for (int c = 0; c < 6; ++c)
             printf("[%llu %llu %llu %llu] ", pp[c][0] % 1000, pp[c][4] % 1000, pp[c][5] % 1000, pp[c][1] % 1000);
         printf("\n");
+        {
+            static unsigned long long se[2][256];
+            static unsigned smid[2048];
+            unsigned nl = 0;
+            cudaMemcpyFromSymbol(se, g_sm_end, sizeof(se));
+            cudaMemcpyFromSymbol(smid, g_smid, sizeof(smid));
+            cudaMemcpyFromSymbol(&nl, g_launch, sizeof(nl));
+            double gap = 0, gmax = 0, red = 0, bor = 0, pw = 0, tail = 0, ex = 0;
+            for (int c = 0; c < G; ++c) {
+                const double g = ((long long)pp[c][0] - (long long)se[nl & 1][smid[c] & 255]) / 1e3;
+                gap += g; gmax = std::max(gmax, g);
+                red += (pp[c][8] - pp[c][2]) / 1e3;
+                bor += (pp[c][9] - pp[c][8]) / 1e3;
+                pw += (pp[c][10] - pp[c][9]) / 1e3;
+                tail += (pp[c][3] - pp[c][10]) / 1e3;
+                ex += (pp[c][7] - pp[c][3]) / 1e3;
+            }
+            printf("pipelined: previous CTA exit on the SM -> this CTA start: avg %.2f max %.2f us\n", gap / G, gmax);
+            {
+                static long long cy[2048][8];
+                cudaMemcpyFromSymbol(cy, g_cyc, sizeof(cy));
+                double d[7] = {0};
+                for (int c = 0; c < G; ++c) {
+                    d[0] += cy[c][0] - cy[c][4]; d[1] += cy[c][1] - cy[c][0]; d[2] += cy[c][2] - cy[c][1];
+                    d[3] += cy[c][3] - cy[c][2]; d[4] += cy[c][5] - cy[c][3]; d[5] += cy[c][6] - cy[c][5];
+                }
+                printf("border cycles (thread 0): slice %.0f, loads %.0f, atomics %.0f, loop end %.0f, return %.0f, barrier %.0f\n",
+                       d[0] / G, d[1] / G, d[2] / G, d[3] / G, d[4] / G, d[5] / G);
+            }
+            printf("pipelined flush split: reduce %.2f, border %.2f, pdl_wait %.2f, combos+REDG %.2f, to exit %.2f us (avg)\n",
+                   red / G, bor / G, pw / G, tail / G, ex / G);
+        }
         printf("pipelined: kernel setup %.2f of ", pk / G);
         printf("pipelined last launch: prologue %.2f, zero loop %.2f, barrier %.2f, main %.2f, flush %.2f us (avg); "
                "first start -> last flush end %.2f us\n", pro / G, zl / G, sy / G, mn / G, fl / G, mx);
@@ -80,7 +112,7 @@ int main(int argc, char** argv)
     }
     std::sort(tot.begin(), tot.end());
     printf("isolated launch (event): median %.2f us\n", tot[reps / 2]);
-    static unsigned long long ph[2048][8];
+    static unsigned long long ph[2048][12];
     cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
     const int G = ctx->last_grid;
     printf("grid %d CTAs\n", G);
