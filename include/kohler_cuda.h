@@ -144,6 +144,16 @@ int kohler_cuda_select_device(kohler_cuda_ctx *ctx, const uint64_t *sums,
 /* Number of kernels the last call on this context launched (bench evidence). */
 int kohler_cuda_last_launch_count(const kohler_cuda_ctx *ctx);
 
+/* Throughput mode for back-to-back device calls on one stream (new in ABI
+ * 1.2; no reference counterpart — the reference has no device pipeline).
+ * depth 1 (default): each accumulation launch spreads over all SMs.  depth d
+ * in [2, 4]: each launch takes ~1/d of the SMs and lets the next one start at
+ * once, so d consecutive calls run side by side and the per-launch fixed
+ * costs overlap; every result is still complete and bit-identical, single
+ * calls just take longer.  Applies to the device batch / band API; the host
+ * API's chunked uploads always use depth 1. */
+int kohler_cuda_set_pipeline_depth(kohler_cuda_ctx *ctx, int depth);
+
 /* label[i] = number of thresholds strictly below px[i] (thresholds sorted
  * ascending, as a ThresholdSet holds them; nts >= 0).  Host buffers; labels
  * is w*h bytes, row-major without padding. */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "kohler_cuda_select_device": (
         _i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kohler_cuda_last_launch_count": (_i, [_vp]),
+    "kohler_cuda_set_pipeline_depth": (_i, [_vp, _i]),
     "kohler_cuda_classify": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
     "kohler_cuda_quantize": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
     "kohler_cuda_segment_batch_device": (

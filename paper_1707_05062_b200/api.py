@@ -187,6 +187,12 @@ class Context:
     def last_launch_count(self) -> int:
         return int(self._lib.kohler_cuda_last_launch_count(self._h))
 
+    def set_pipeline_depth(self, depth: int) -> None:
+        """Throughput mode for back-to-back device calls (include/kohler_cuda.h):
+        depth d in [1, 4] accumulation launches run side by side on 1/d of the
+        SMs each.  Results are unchanged."""
+        _raise_for(self._lib.kohler_cuda_set_pipeline_depth(self._h, int(depth)))
+
     # ---- host-memory API ------------------------------------------------
     def curve(self, px: np.ndarray) -> ContrastCurve:
         px = np.ascontiguousarray(px, dtype=np.uint8)

@@ -33,6 +33,7 @@ using namespace kohler_dev;
 namespace {
 
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
+constexpr int kMaxDepth = 4;         // K1 launches in flight (pipelined mode)
 constexpr int kMaxSelectLevels = 4096;
 
 struct WideParams {
@@ -60,6 +61,7 @@ struct WideParams {
     int k;
     int select;
     int no_finish;  // accumulate only (a band of a chunked image; a later launch finishes)
+    int early_trigger;  // pipelined launches: let the next launch start at once (disjoint SMs)
     uint32_t* hist_out;  // [n][256] pixel histogram (atomically accumulated), or null
     uint64_t* sums;
     uint64_t* cards;
@@ -780,6 +782,8 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
     // on them would otherwise serialise one miss per line.
     asm volatile("" ::"l"(p.px), "r"(p.band_rows), "l"(p.T), "r"(p.epoch), "l"(p.cta_q),
                  "l"(p.acc), "l"(p.hist_out), "l"(p.t0s), "l"(p.status));
+    if (p.early_trigger)
+        pdl_trigger();  // pipeline depth > 1: the next launch takes the SMs this grid leaves free
     const long long rb = blockIdx.x;
     const long long cs = rb * p.cta_q + (rb < p.cta_r ? rb : p.cta_r);
     const long long ce = cs + p.cta_q + (rb < p.cta_r ? 1 : 0);
@@ -1695,6 +1699,7 @@ struct kohler_cuda_ctx {
     DevBuf seg;      // segmentation scratch (histograms, thresholds)
     int last_launches = 0;
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
+    int depth = 1;      // K1 launches in flight (kohler_cuda_set_pipeline_depth)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };
@@ -1773,7 +1778,15 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     if (pitch >= (1ull << 31) / 64)
         return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
     const int nseg = (w + 15) / 16;
-    const int G_max = std::max(1, ctx->sm_count - 1);
+    // Pipeline depth d > 1 (finishing launches only): each K1 takes 1/d of
+    // the SMs (one more per launch for its finish_kernel) and triggers its
+    // successor at once, so d consecutive launches run side by side and each
+    // one's prologue / zeroing / flush / launch gap hides under the others'
+    // walks.  One accumulator buffer suffices: a launch's flush REDGs only
+    // after its griddepcontrol.wait, i.e. after the previous launch's
+    // finish_kernel has read and reset the buffer.
+    const int depth = no_finish ? 1 : std::max(1, ctx->depth);
+    const int G_max = depth > 1 ? std::max(1, (ctx->sm_count - depth) / depth) : std::max(1, ctx->sm_count - 1);
     // Rows per column walk R: a walk's rows past the band end still cost
     // their steps, so prefer R dividing the band height; longer walks
     // amortise the per-segment prime row.
@@ -1843,6 +1856,7 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         p.epoch = two_w ? (int)std::max(1.0, std::floor(cap2 / (0.5 + 1.5 / (double)R))) : (int)e1;
     }
     p.acc = static_cast<unsigned long long*>(ctx->acc.p);
+    p.early_trigger = depth > 1 ? 1 : 0;
     p.copies = copies;
     p.tickets = static_cast<unsigned*>(ctx->tickets.p);
     p.cta_q = U / G;
@@ -2399,7 +2413,7 @@ int segment_device(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h,
 
 extern "C" {
 
-int kohler_cuda_abi_version(void) { return 100; }
+int kohler_cuda_abi_version(void) { return 101; }
 
 const char* kohler_cuda_last_error(void) { return g_last_error.c_str(); }
 
@@ -2469,6 +2483,17 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
 int kohler_cuda_device(const kohler_cuda_ctx* ctx) { return ctx ? ctx->device : -1; }
 
 int kohler_cuda_last_launch_count(const kohler_cuda_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int kohler_cuda_set_pipeline_depth(kohler_cuda_ctx* ctx, int depth)
+{
+    if (!ctx)
+        return fail(KOHLER_INVALID_ARGUMENT, "null context");
+    if (depth < 1 || depth > kMaxDepth)
+        return fail(KOHLER_INVALID_ARGUMENT, "pipeline depth must be in [1, 4]");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->depth = depth;
+    return KOHLER_OK;
+}
 
 int kohler_cuda_curve(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,
                       uint64_t* sum, uint64_t* card)

@@ -148,3 +148,45 @@ def test_host_api_chunked_batch_vs_reference(ctx, ref):
     r = host_result(ctx.analyze_batch(x, K))
     exp = ref.analyze_batch(x, K, workers=1)
     check_against_reference(r, exp)
+
+
+@pytest.mark.parametrize("depth", [2, 3, 4])
+def test_pipelined_back_to_back_calls(ref, depth):
+    """Pipeline depth d (kohler_cuda_set_pipeline_depth): d consecutive
+    accumulation launches run side by side (sharing one accumulator buffer:
+    each flush waits for the previous finish_kernel).  Back-to-back calls on different images must give exactly the
+    depth-1 results (and the reference's on the C2 image)."""
+    from paper_1707_05062_b200 import Context
+    x = synth.generate("C2", device="cuda")[0]
+    imgs = [x, x.flip(0).contiguous(), x.flip(1).contiguous(), (255 - x).contiguous(),
+            x[:, :4000].contiguous(), x[::2].contiguous(), x.t().contiguous()]
+    c1 = Context(0)
+    want = [run_batch(c1, im[None]) for im in imgs]
+    cp = Context(0)
+    cp.set_pipeline_depth(depth)
+    outs = []
+    for rep in range(2):
+        for im in imgs:  # no synchronisation between the calls
+            h, w = im.shape
+            o = {"sums": torch.zeros((1, 256), dtype=torch.int64, device="cuda"),
+                 "cards": torch.zeros((1, 256), dtype=torch.int64, device="cuda"),
+                 "values": torch.zeros((1, 256), dtype=torch.float64, device="cuda"),
+                 "defined": torch.zeros((1, 256), dtype=torch.uint8, device="cuda"),
+                 "t0": torch.zeros(1, dtype=torch.int32, device="cuda"),
+                 "topk": torch.zeros((1, K), dtype=torch.int32, device="cuda"),
+                 "topk_count": torch.zeros(1, dtype=torch.int32, device="cuda"),
+                 "status": torch.zeros(1, dtype=torch.int32, device="cuda")}
+            cp.analyze_batch_device(im, w, h, w, w * h, 1, K, o)
+            outs.append(o)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        e = want[i % len(imgs)]
+        for key in ("sums", "cards", "values", "t0", "topk", "topk_count", "status"):
+            got = o[key].cpu().numpy()
+            if key in ("sums", "cards"):
+                got = got.view(np.uint64)
+            assert np.array_equal(got, e[key]), (i, key)
+    exp = ref.analyze_batch(x.cpu().numpy()[None], K)
+    check_against_reference(want[0], exp)
+    with pytest.raises(ValueError):
+        cp.set_pipeline_depth(5)

@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--depth", type=int, default=1, help="kohler_cuda_set_pipeline_depth")
 ap.add_argument("--segment", type=int, default=-1,
                 help=">= 0: time the segmentation pipeline instead (0: curve -> {t0} -> "
                      "two-class quantize per image, bench.cpp:266-281; k: top-k quantize)")
@@ -30,6 +31,7 @@ if x.numel() < 2 * l2:  # rotate copies so every step reads HBM
 else:
     x = x[None]
 ctx = Context(0)
+ctx.set_pipeline_depth(a.depth)
 k = 6
 out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
        "cards": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
@@ -62,7 +64,7 @@ if a.time:
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
     px = n * h * w
-    print(json.dumps({"config": a.config, "segment": a.segment, "n": n, "w": w, "h": h,
+    print(json.dumps({"config": a.config, "depth": a.depth, "segment": a.segment, "n": n, "w": w, "h": h,
                       "ms_per_step": ms,
                       "gpix_per_s": px / ms / 1e6, "hbm_frac": px / ms / 1e6 / 6452.8,
                       "images_per_s": n / ms * 1e3, "copies": copies, "steps": steps}))
