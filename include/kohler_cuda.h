@@ -154,6 +154,36 @@ int kohler_cuda_last_launch_count(const kohler_cuda_ctx *ctx);
  * API's chunked uploads always use depth 1. */
 int kohler_cuda_set_pipeline_depth(kohler_cuda_ctx *ctx, int depth);
 
+/* ---- colour ingest (ABI 1.1) ------------------------------------------
+ * Rec. 601 integer luma of interleaved 8-bit RGB, bit-identical to the
+ * reference's luma601 (proj/src/pnm.cpp:63-68) that read_pnm applies to
+ * P6 / P3 input (pnm.cpp:110-136):
+ *     gray = min((299 r + 587 g + 114 b + 500) / 1000, 255)
+ * rgb_pitch (>= 3 * w) and rgb_stride are in bytes. */
+
+/* Host buffers; blocks until gray (w x h, row pitch gray_pitch) is written. */
+int kohler_cuda_rgb_to_gray(kohler_cuda_ctx *ctx, const uint8_t *rgb, int w, int h,
+                            size_t rgb_pitch, uint8_t *gray, size_t gray_pitch);
+
+/* Device buffers, asynchronous on `stream`. */
+int kohler_cuda_rgb_to_gray_device(kohler_cuda_ctx *ctx, const uint8_t *rgb, int n, int w, int h,
+                                   size_t rgb_pitch, size_t rgb_stride, uint8_t *gray,
+                                   size_t gray_pitch, size_t gray_stride, void *stream);
+
+/* The full per-image pipeline of kohler_cuda_analyze_batch on RGB input:
+ * fast_contrast_curve(read_pnm(P6 bytes)) + mean_contrast + optimal_threshold
+ * + top_k_local_maxima in one call, the grey image existing only in device
+ * staging memory.  Host buffers (synchronous) / device buffers (on `stream`). */
+int kohler_cuda_analyze_rgb_batch(kohler_cuda_ctx *ctx, const uint8_t *rgb, int n, int w, int h,
+                                  size_t rgb_pitch, size_t rgb_stride, int k, uint64_t *sums,
+                                  uint64_t *cards, double *values, uint8_t *defined, int *t0s,
+                                  int *topks, int *topk_counts, int *status);
+int kohler_cuda_analyze_rgb_batch_device(kohler_cuda_ctx *ctx, const uint8_t *rgb, int n, int w,
+                                         int h, size_t rgb_pitch, size_t rgb_stride, int k,
+                                         uint64_t *sums, uint64_t *cards, double *values,
+                                         uint8_t *defined, int *t0s, int *topks,
+                                         int *topk_counts, int *status, void *stream);
+
 /* label[i] = number of thresholds strictly below px[i] (thresholds sorted
  * ascending, as a ThresholdSet holds them; nts >= 0).  Host buffers; labels
  * is w*h bytes, row-major without padding. */

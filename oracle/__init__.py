@@ -60,6 +60,7 @@ class Oracle:
             ("oracle_top_k_local_maxima", [vp, vp, i, i, vp, vp], i),
             ("oracle_identities", [vp, i, i, vp, vp], None),
             ("oracle_analyze", [vp, i, i, i, vp, vp, vp, vp, vp, vp, vp], i),
+            ("oracle_rgb_to_gray", [vp, i, i, C.c_size_t, vp], None),
         ]:
             f = getattr(self.lib, name)
             f.argtypes = args
@@ -71,6 +72,16 @@ class Oracle:
         if px.ndim != 2:
             raise ValueError("expected a 2-D image")
         return px, px.shape[1], px.shape[0]
+
+    def rgb_to_gray(self, rgb):
+        """rgb: (h, w, 3) uint8 -> (h, w) luma (pnm.cpp:63-68 restated)."""
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        if rgb.ndim != 3 or rgb.shape[2] != 3:
+            raise ValueError("expected an (h, w, 3) RGB image")
+        h, w = rgb.shape[:2]
+        out = np.empty((h, w), np.uint8)
+        self.lib.oracle_rgb_to_gray(_p(rgb), w, h, 3 * w, _p(out))
+        return out
 
     def pair_contribution(self, lo, hi):
         s = np.zeros(256, np.uint64)
@@ -177,10 +188,23 @@ class Reference:
             ("kref_classify", [vp, vp, i, vp], None),
             ("kref_quantize", [vp, vp, i, vp], None),
             ("kref_segment", [vp, u, i, vp, vp, vp], i),
+            ("kref_read_pnm", [vp, C.c_size_t, vp, C.c_size_t, vp, vp], i),
         ]:
             f = getattr(self.lib, name)
             f.argtypes = args
             f.restype = res
+
+    def read_pnm(self, data: bytes) -> np.ndarray:
+        """The reference's read_pnm (proj/src/pnm.cpp:87-139) on a PNM byte
+        stream -> (h, w) uint8; ValueError on a PnmError."""
+        buf = np.frombuffer(bytes(data), np.uint8)
+        cap = max(len(data), 1)
+        out = np.empty(cap, np.uint8)
+        w, h = C.c_int(0), C.c_int(0)
+        rc = self.lib.kref_read_pnm(_p(buf), len(data), _p(out), cap, C.byref(w), C.byref(h))
+        if rc:
+            raise ValueError("reference read_pnm rejected the stream")
+        return out[: w.value * h.value].reshape(h.value, w.value).copy()
 
     def active_kernel(self) -> str:
         return self.lib.kref_active_kernel().decode()

@@ -261,3 +261,22 @@ int oracle_analyze(const uint8_t *px, int w, int h, int k, uint64_t *sum, uint64
     *t0 = oracle_optimal_threshold(values, defined, ORACLE_LEVELS);
     return oracle_top_k_local_maxima(values, defined, ORACLE_LEVELS, k, topk, topk_count);
 }
+
+/* Rec. 601 integer luma of one RGB sample, as the reference's luma601
+ * (proj/src/pnm.cpp:63-68): round half up in thousandths, clamped to 255. */
+uint8_t oracle_luma601(unsigned r, unsigned g, unsigned b)
+{
+    const unsigned v = (299u * r + 587u * g + 114u * b + 500u) / 1000u;
+    return (uint8_t)(v < 255u ? v : 255u);
+}
+
+/* Colour reduction of read_pnm for P6 / P3 (proj/src/pnm.cpp:110-136):
+ * interleaved RGB rows of `pitch` bytes -> w x h grey, row-major. */
+void oracle_rgb_to_gray(const uint8_t *rgb, int w, int h, size_t pitch, uint8_t *out)
+{
+    for (int y = 0; y < h; ++y) {
+        const uint8_t *row = rgb + (size_t)y * pitch;
+        for (int x = 0; x < w; ++x)
+            out[(size_t)y * w + x] = oracle_luma601(row[3 * x], row[3 * x + 1], row[3 * x + 2]);
+    }
+}

@@ -27,6 +27,8 @@ int oracle_optimal_threshold(const double *values, const uint8_t *defined, int n
 int oracle_top_k_local_maxima(const double *values, const uint8_t *defined, int n, int k,
                               int *out, int *out_count);
 void oracle_identities(const uint8_t *px, int w, int h, uint64_t *tv, uint64_t *qs);
+uint8_t oracle_luma601(unsigned r, unsigned g, unsigned b);
+void oracle_rgb_to_gray(const uint8_t *rgb, int w, int h, size_t pitch, uint8_t *out);
 int oracle_analyze(const uint8_t *px, int w, int h, int k, uint64_t *sum, uint64_t *card,
                    double *values, uint8_t *defined, int *t0, int *topk, int *topk_count);
 

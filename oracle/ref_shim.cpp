@@ -22,6 +22,7 @@
 #include "kohler/curve.hpp"
 #include "kohler/image.hpp"
 #include "kohler/kernels.hpp"
+#include "kohler/pnm.hpp"
 #include "kohler/threshold.hpp"
 
 namespace {
@@ -285,6 +286,25 @@ int kref_segment(const void* img, unsigned workers, int k, uint8_t* out, int* ts
         const auto px = im.pixels();
         std::copy(px.begin(), px.end(), out);
         return 1;
+    }
+}
+
+// The reference's PNM decoder (proj/src/pnm.cpp:87-139): pins the colour
+// ingest (luma601 on P6 / P3) of the CUDA path.  0 ok, 2 on a PnmError or if
+// the image does not fit `cap` bytes.
+int kref_read_pnm(const uint8_t* bytes, size_t n, uint8_t* out, size_t cap, int* w, int* h)
+{
+    try {
+        const kohler::GrayImage im = kohler::read_pnm(std::span<const std::uint8_t>(bytes, n));
+        const auto px = im.pixels();
+        if (px.size() > cap)
+            return 2;
+        std::copy(px.begin(), px.end(), out);
+        *w = im.width();
+        *h = im.height();
+        return 0;
+    } catch (const std::exception&) {
+        return 2;
     }
 }
 

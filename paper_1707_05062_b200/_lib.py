@@ -52,6 +52,12 @@ SIGNATURES = {
         _i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kohler_cuda_last_launch_count": (_i, [_vp]),
     "kohler_cuda_set_pipeline_depth": (_i, [_vp, _i]),
+    "kohler_cuda_rgb_to_gray": (_i, [_vp, _vp, _i, _i, _sz, _vp, _sz]),
+    "kohler_cuda_rgb_to_gray_device": (_i, [_vp, _vp, _i, _i, _i, _sz, _sz, _vp, _sz, _sz, _vp]),
+    "kohler_cuda_analyze_rgb_batch": (
+        _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kohler_cuda_analyze_rgb_batch_device": (
+        _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kohler_cuda_classify": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
     "kohler_cuda_quantize": (_i, [_vp, _vp, _i, _i, _sz, _vp, _i, _vp]),
     "kohler_cuda_segment_batch_device": (

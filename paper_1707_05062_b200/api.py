@@ -286,6 +286,49 @@ class Context:
             _stream(stream)))
 
 
+    # ---- colour ingest ------------------------------
+    def rgb_to_gray(self, rgb: np.ndarray) -> np.ndarray:
+        """Rec. 601 integer luma of an (h, w, 3) u8 image on the GPU, as the
+        reference's read_pnm reduces P6/P3 input (pnm.cpp:63-68)."""
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        if rgb.ndim != 3 or rgb.shape[2] != 3:
+            raise ValueError("expected an (h, w, 3) RGB image")
+        h, w = rgb.shape[:2]
+        out = np.empty((h, w), np.uint8)
+        _raise_for(self._lib.kohler_cuda_rgb_to_gray(self._h, _ptr(rgb), w, h, 3 * w, _ptr(out), w))
+        return out
+
+    def rgb_to_gray_device(self, rgb, n: int, w: int, h: int, rgb_pitch: int, rgb_stride: int,
+                           gray, gray_pitch: int, gray_stride: int, stream=None) -> None:
+        _raise_for(self._lib.kohler_cuda_rgb_to_gray_device(
+            self._h, _dptr(rgb), int(n), int(w), int(h), int(rgb_pitch), int(rgb_stride),
+            _dptr(gray), int(gray_pitch), int(gray_stride), _stream(stream)))
+
+    def analyze_rgb_batch(self, rgb: np.ndarray, k: int = 6, curves: bool = True,
+                          mean: bool = True) -> BatchResult:
+        """analyze_batch on RGB input rgb[n, h, w, 3] (or [h, w, 3]): the
+        luma is computed on the GPU and never leaves device staging memory."""
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        if rgb.ndim == 3:
+            rgb = rgb[None]
+        if rgb.ndim != 4 or rgb.shape[3] != 3:
+            raise ValueError("expected RGB images of shape (n, h, w, 3)")
+        n, h, w = rgb.shape[:3]
+        r = _alloc_result(n, k, curves, mean)
+        _raise_for(self._lib.kohler_cuda_analyze_rgb_batch(
+            self._h, _ptr(rgb), n, w, h, 3 * w, 3 * w * h, int(k),
+            _optr(r.sums), _optr(r.cards), _optr(r.values), _optr(r.defined),
+            _ptr(r.t0), _ptr(r.topk), _ptr(r.topk_count), _ptr(r.status)))
+        return r
+
+    def analyze_rgb_batch_device(self, rgb, w: int, h: int, rgb_pitch: int, rgb_stride: int,
+                                 n: int, k: int, out: dict, stream=None) -> None:
+        _raise_for(self._lib.kohler_cuda_analyze_rgb_batch_device(
+            self._h, _dptr(rgb), int(n), int(w), int(h), int(rgb_pitch), int(rgb_stride), int(k),
+            _dptr(out.get("sums")), _dptr(out.get("cards")), _dptr(out.get("values")),
+            _dptr(out.get("defined")), _dptr(out.get("t0")), _dptr(out.get("topk")),
+            _dptr(out.get("topk_count")), _dptr(out.get("status")), _stream(stream)))
+
     # ---- segmentation (SURVEY.md §8f rank 1) -------------------------------
     def classify(self, px: np.ndarray, thresholds) -> np.ndarray:
         """labels[y, x] = number of thresholds strictly below px[y, x]."""

@@ -1651,6 +1651,76 @@ struct HostBuf {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Colour ingest: Rec. 601 integer luma of interleaved
+// RGB, exactly the reference's luma601 (proj/src/pnm.cpp:63-68), used by
+// read_pnm for P6/P3 input (:110-136):
+//     v = min((299 r + 587 g + 114 b + 500) / 1000, 255)
+// HBM-bound (3 B read + 1 B written per pixel).  One thread converts 16
+// pixels: three 16-byte loads, the weighted sums by two DP2A per pixel
+// (16-bit weights x 8-bit samples, FMA pipe), the division by 1000 as one
+// IMAD.HI with ceil(2^32 / 1000) (exact for t < 2^18: 704 t < 2^32), one
+// 16-byte store.  Ragged row ends / unaligned buffers take a per-pixel loop.
+// ---------------------------------------------------------------------------
+struct LumaParams {
+    const uint8_t* rgb;
+    size_t rpitch, rstride;   // bytes between rows / images of the RGB input
+    uint8_t* gray;
+    size_t gpitch, gstride;
+    int w, rows, n;
+    int vec;                  // all bases / pitches / strides 16-byte aligned
+    long long items;          // n * rows * ceil(w / 16)
+    int nchunk;
+};
+
+constexpr uint32_t kLumaMagic = 4294968u;  // ceil(2^32 / 1000)
+
+__device__ __forceinline__ uint32_t luma_div(uint32_t t) { return __umulhi(t, kLumaMagic); }
+
+__device__ __forceinline__ uint32_t luma1(uint32_t r, uint32_t g, uint32_t b)
+{
+    return luma_div(299u * r + 587u * g + 114u * b + 500u);
+}
+
+// four pixels from three words r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3 -> packed bytes
+__device__ __forceinline__ uint32_t luma4(uint32_t w0, uint32_t w1, uint32_t w2)
+{
+    constexpr uint32_t A = 299u | 587u << 16, B = 114u, C = 299u << 16, D = 587u | 114u << 16;
+    const uint32_t p0 = luma_div(__dp2a_hi(B, w0, __dp2a_lo(A, w0, 500u)));
+    const uint32_t p1 = luma_div(__dp2a_lo(D, w1, __dp2a_hi(C, w0, 500u)));
+    const uint32_t p2 = luma_div(__dp2a_lo(B, w2, __dp2a_hi(A, w1, 500u)));
+    const uint32_t p3 = luma_div(__dp2a_hi(D, w2, __dp2a_lo(C, w2, 500u)));
+    return __byte_perm(p0 | p1 << 8, p2 | p3 << 8, 0x5410);
+}
+
+__global__ void __launch_bounds__(256) luma_kernel(const LumaParams p)
+{
+    for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < p.items;
+         it += (long long)gridDim.x * blockDim.x) {
+        const long long rowi = it / p.nchunk;
+        const int c = (int)(it - rowi * p.nchunk);
+        const int img = (int)(rowi / p.rows), y = (int)(rowi - (long long)img * p.rows);
+        const uint8_t* src = p.rgb + (size_t)img * p.rstride + (size_t)y * p.rpitch + (size_t)c * 48;
+        uint8_t* dst = p.gray + (size_t)img * p.gstride + (size_t)y * p.gpitch + (size_t)c * 16;
+        const int x0 = c * 16;
+        if (p.vec && x0 + 16 <= p.w) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+            const uint4 d = __ldg(reinterpret_cast<const uint4*>(src) + 2);
+            uint4 o;
+            o.x = luma4(a.x, a.y, a.z);
+            o.y = luma4(a.w, b.x, b.y);
+            o.z = luma4(b.z, b.w, d.x);
+            o.w = luma4(d.y, d.z, d.w);
+            *reinterpret_cast<uint4*>(dst) = o;
+        } else {
+            const int e = min(16, p.w - x0);
+            for (int i = 0; i < e; ++i)
+                dst[i] = (uint8_t)luma1(src[3 * i], src[3 * i + 1], src[3 * i + 2]);
+        }
+    }
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -1696,6 +1766,8 @@ struct kohler_cuda_ctx {
     DevBuf curves;   // K5 curve scratch when the caller wants no curves
     DevBuf stage;    // 16-byte aligned copy of unaligned device inputs for K1
     HostBuf hout;    // pinned staging for small results (one D2H per call)
+    DevBuf rgb;      // staging for host RGB images (colour ingest)
+    DevBuf gray;     // luma of device RGB inputs (16-byte pitched)
     DevBuf seg;      // segmentation scratch (histograms, thresholds)
     int last_launches = 0;
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
@@ -1733,6 +1805,46 @@ struct BatchOut {
     int* topk_counts;
     int* status;
 };
+
+int launch_luma(kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, int rows, size_t rpitch,
+                size_t rstride, uint8_t* gray, size_t gpitch, size_t gstride, cudaStream_t st)
+{
+    if (n <= 0 || rows <= 0)
+        return KOHLER_OK;
+    LumaParams lp{};
+    lp.rgb = rgb;
+    lp.rpitch = rpitch;
+    lp.rstride = rstride;
+    lp.gray = gray;
+    lp.gpitch = gpitch;
+    lp.gstride = gstride;
+    lp.w = w;
+    lp.rows = rows;
+    lp.n = n;
+    lp.nchunk = (w + 15) / 16;
+    lp.items = (long long)n * rows * lp.nchunk;
+    auto al = [](uintptr_t x) { return x % 16 == 0; };
+    lp.vec = al((uintptr_t)rgb) && al(rpitch) && (n == 1 || al(rstride)) && al((uintptr_t)gray) &&
+             al(gpitch) && (n == 1 || al(gstride));
+    const long long blocks = std::min<long long>((lp.items + 255) / 256, (long long)ctx->sm_count * 8);
+    luma_kernel<<<(unsigned)blocks, 256, 0, st>>>(lp);
+    KC_CUDA(cudaGetLastError());
+    ctx->last_launches += 1;
+    return KOHLER_OK;
+}
+
+int check_rgb(int n, int w, int h, size_t pitch, size_t stride)
+{
+    if (n < 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "image count must be >= 0");
+    if (w < 1 || h < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "GrayImage: dimensions must be at least 1x1");
+    if (pitch < 3 * (size_t)w)
+        return fail(KOHLER_INVALID_ARGUMENT, "RGB row pitch must be >= 3 * width");
+    if (n > 1 && stride < pitch * (size_t)h)
+        return fail(KOHLER_INVALID_ARGUMENT, "image stride smaller than one image");
+    return KOHLER_OK;
+}
 
 int check_image(int n, int w, int h, size_t pitch)
 {
@@ -2112,7 +2224,7 @@ bool use_tile(int n, int w, int h) { return n >= 2 && (long long)w * h <= 65536;
 // into two contiguous image ranges.  Small results come back in ONE
 // device-to-host copy.
 int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
-               size_t image_stride, int k, int select, const BatchOut& host)
+               size_t image_stride, int k, int select, const BatchOut& host, int channels = 1)
 {
     const size_t dpitch = round_up((size_t)w, 16);
     const size_t dstride = dpitch * (size_t)h;
@@ -2120,6 +2232,17 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     if (rc)
         return rc;
     uint8_t* dimg = static_cast<uint8_t*>(ctx->img.p);
+    // uploads land in dimg (grey) or, for RGB input, in the RGB staging
+    // buffer, converted per chunk by luma_kernel into dimg
+    const size_t wb = (size_t)w * channels;
+    const size_t upitch = channels == 1 ? dpitch : round_up(wb, 16);
+    const size_t ustride = upitch * (size_t)h;
+    if (channels != 1) {
+        rc = ctx->rgb.ensure(std::max<size_t>(ustride * (size_t)n, 16));
+        if (rc)
+            return rc;
+    }
+    uint8_t* dup = channels == 1 ? dimg : static_cast<uint8_t*>(ctx->rgb.p);
     cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     // device outputs, packed: sums | cards | values | defined | t0 | count | status | topk
     const size_t n256 = (size_t)n * 256;
@@ -2144,22 +2267,29 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     auto upload = [&](int i0, int i1, int y0, int y1) -> int {
         // images [i0, i1), rows [y0, y1) of each
         const size_t rows = (size_t)(y1 - y0);
-        if (pitch == dpitch && (i1 - i0 == 1 || image_stride == pitch * (size_t)h)) {
-            const size_t off = (size_t)i0 * dstride + (size_t)y0 * dpitch;
-            const size_t len = (i1 - i0 == 1) ? rows * dpitch : (size_t)(i1 - i0) * dstride;
-            KC_CUDA(cudaMemcpyAsync(dimg + off, px + (size_t)i0 * image_stride + (size_t)y0 * pitch,
+        if (pitch == upitch && (i1 - i0 == 1 || image_stride == pitch * (size_t)h)) {
+            const size_t off = (size_t)i0 * ustride + (size_t)y0 * upitch;
+            const size_t len = (i1 - i0 == 1) ? rows * upitch : (size_t)(i1 - i0) * ustride;
+            KC_CUDA(cudaMemcpyAsync(dup + off, px + (size_t)i0 * image_stride + (size_t)y0 * pitch,
                                     len, cudaMemcpyHostToDevice, cs));
         } else if (image_stride == pitch * (size_t)h && y0 == 0 && y1 == h) {
-            KC_CUDA(cudaMemcpy2DAsync(dimg + (size_t)i0 * dstride, dpitch,
-                                      px + (size_t)i0 * image_stride, pitch, (size_t)w,
+            KC_CUDA(cudaMemcpy2DAsync(dup + (size_t)i0 * ustride, upitch,
+                                      px + (size_t)i0 * image_stride, pitch, wb,
                                       (size_t)h * (i1 - i0), cudaMemcpyHostToDevice, cs));
         } else {
             for (int i = i0; i < i1; ++i)
-                KC_CUDA(cudaMemcpy2DAsync(dimg + dstride * i + (size_t)y0 * dpitch, dpitch,
+                KC_CUDA(cudaMemcpy2DAsync(dup + ustride * i + (size_t)y0 * upitch, upitch,
                                           px + image_stride * i + (size_t)y0 * pitch, pitch,
-                                          (size_t)w, rows, cudaMemcpyHostToDevice, cs));
+                                          wb, rows, cudaMemcpyHostToDevice, cs));
         }
         return KOHLER_OK;
+    };
+    auto to_gray = [&](int i0, int i1, int y0, int y1) -> int {
+        if (channels == 1)
+            return KOHLER_OK;
+        return launch_luma(ctx, dup + (size_t)i0 * ustride + (size_t)y0 * upitch, i1 - i0, w,
+                           y1 - y0, upitch, ustride, dimg + (size_t)i0 * dstride + (size_t)y0 * dpitch,
+                           dpitch, dstride, st);
     };
     auto sub = [&](int i0) {
         BatchOut s = d;
@@ -2192,6 +2322,9 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
                 return rc;
             KC_CUDA(cudaEventRecord(ctx->chunk_ev[c], cs));
             KC_CUDA(cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
+            rc = to_gray(0, 1, a, std::min(e + 1, h));
+            if (rc)
+                return rc;
             rc = launch_wide(ctx, dimg + (size_t)a * dpitch, 1, w, e - a, h, a, dpitch, dstride, k,
                              select, d, st, c + 1 < chunks ? 1 : 0);
         } else {
@@ -2201,6 +2334,9 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
                 return rc;
             KC_CUDA(cudaEventRecord(ctx->chunk_ev[c], cs));
             KC_CUDA(cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
+            rc = to_gray(i0, i1, 0, h);
+            if (rc)
+                return rc;
             const uint8_t* src = dimg + (size_t)i0 * dstride;
             rc = tile ? launch_tile(ctx, src, i1 - i0, w, h, dpitch, dstride, k, select, sub(i0), st)
                       : launch_wide(ctx, src, i1 - i0, w, h, h, 0, dpitch, dstride, k, select,
@@ -2468,6 +2604,8 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         ctx->stage.release();
         ctx->hout.release();
         ctx->seg.release();
+        ctx->rgb.release();
+        ctx->gray.release();
         cudaStreamDestroy(ctx->stream);
         if (ctx->copy_stream)
             cudaStreamDestroy(ctx->copy_stream);
@@ -2597,6 +2735,111 @@ int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, in
                            static_cast<cudaStream_t>(stream));
     return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select ? 1 : 0, o,
                        static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_rgb_to_gray_device(kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, int h,
+                                   size_t rgb_pitch, size_t rgb_stride, uint8_t* gray,
+                                   size_t gray_pitch, size_t gray_stride, void* stream)
+{
+    if (!ctx || ((!rgb || !gray) && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_rgb(n, w, h, rgb_pitch, rgb_stride);
+    if (rc)
+        return rc;
+    if (gray_pitch < (size_t)w || (n > 1 && gray_stride < gray_pitch * (size_t)h))
+        return fail(KOHLER_INVALID_ARGUMENT, "grey pitch / stride too small");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    return launch_luma(ctx, rgb, n, w, h, rgb_pitch, rgb_stride, gray, gray_pitch, gray_stride,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_rgb_to_gray(kohler_cuda_ctx* ctx, const uint8_t* rgb, int w, int h,
+                            size_t rgb_pitch, uint8_t* gray, size_t gray_pitch)
+{
+    if (!ctx || !rgb || !gray)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_rgb(1, w, h, rgb_pitch, 0);
+    if (rc)
+        return rc;
+    if (gray_pitch < (size_t)w)
+        return fail(KOHLER_INVALID_ARGUMENT, "grey pitch must be >= width");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    const size_t up = round_up(3 * (size_t)w, 16), dp = round_up((size_t)w, 16);
+    rc = ctx->rgb.ensure(up * (size_t)h);
+    if (rc)
+        return rc;
+    rc = ctx->gray.ensure(dp * (size_t)h);
+    if (rc)
+        return rc;
+    uint8_t* drgb = static_cast<uint8_t*>(ctx->rgb.p);
+    uint8_t* dg = static_cast<uint8_t*>(ctx->gray.p);
+    cudaStream_t st = ctx->stream;
+    KC_CUDA(cudaMemcpy2DAsync(drgb, up, rgb, rgb_pitch, 3 * (size_t)w, (size_t)h,
+                              cudaMemcpyHostToDevice, st));
+    rc = launch_luma(ctx, drgb, 1, w, h, up, up * (size_t)h, dg, dp, dp * (size_t)h, st);
+    if (rc)
+        return rc;
+    KC_CUDA(cudaMemcpy2DAsync(gray, gray_pitch, dg, dp, (size_t)w, (size_t)h, cudaMemcpyDeviceToHost,
+                              st));
+    KC_CUDA(cudaStreamSynchronize(st));
+    return KOHLER_OK;
+}
+
+int kohler_cuda_analyze_rgb_batch(kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, int h,
+                                  size_t rgb_pitch, size_t rgb_stride, int k, uint64_t* sums,
+                                  uint64_t* cards, double* values, uint8_t* defined, int* t0s,
+                                  int* topks, int* topk_counts, int* status)
+{
+    if (!ctx || (!rgb && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_rgb(n, w, h, rgb_pitch, rgb_stride);
+    if (rc)
+        return rc;
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
+    return host_batch(ctx, rgb, n, w, h, rgb_pitch, n > 1 ? rgb_stride : rgb_pitch * (size_t)h, k, 1,
+                      o, 3);
+}
+
+int kohler_cuda_analyze_rgb_batch_device(kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w,
+                                         int h, size_t rgb_pitch, size_t rgb_stride, int k,
+                                         uint64_t* sums, uint64_t* cards, double* values,
+                                         uint8_t* defined, int* t0s, int* topks, int* topk_counts,
+                                         int* status, void* stream)
+{
+    if (!ctx || (!rgb && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_rgb(n, w, h, rgb_pitch, rgb_stride);
+    if (rc)
+        return rc;
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (n == 0)
+        return KOHLER_OK;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    ctx->last_launches = 0;
+    const size_t dp = round_up((size_t)w, 16), ds = dp * (size_t)h;
+    rc = ctx->gray.ensure(ds * (size_t)n);
+    if (rc)
+        return rc;
+    uint8_t* dg = static_cast<uint8_t*>(ctx->gray.p);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    rc = launch_luma(ctx, rgb, n, w, h, rgb_pitch, rgb_stride, dg, dp, ds, st);
+    if (rc)
+        return rc;
+    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
+    const bool select = t0s || topks || topk_counts || status;
+    if (use_tile(n, w, h))
+        return launch_tile(ctx, dg, n, w, h, dp, ds, k, select ? 1 : 0, o, st);
+    return launch_wide(ctx, dg, n, w, h, h, 0, dp, ds, k, select ? 1 : 0, o, st);
 }
 
 int kohler_cuda_classify(kohler_cuda_ctx* ctx, const uint8_t* px, int w, int h, size_t pitch,

@@ -12,7 +12,11 @@ proj/tests/acceptance.cpp:86-103 and test_support.hpp:20-68) with the curves,
 mean curves, optimal thresholds and top-6 maxima the reference library
 computes for them, and tests/golden/selection.npz: synthetic mean curves
 (plateaus, undefined gaps, ties) with the reference's optimal_threshold and
-top_k_local_maxima for k in 1..8.
+top_k_local_maxima for k in 1..8, and tests/golden/luma.npz (colour
+ingest): RGB samples / a seeded RGB image encoded as P6 and P3 streams and
+decoded by the reference's read_pnm (proj/src/pnm.cpp:87-139, luma601 at
+:63-68), plus the reference pipeline on the decoded image
+(``python tests/golden/make_golden.py --luma-only`` rewrites only this file).
 """
 from __future__ import annotations
 
@@ -86,8 +90,45 @@ def synthetic_curves(seed: int = 0x5E1EC7, count: int = 300):
     return np.array(vals), np.array(defs)
 
 
+def luma_golden(ref) -> None:
+    rng = np.random.default_rng(0x601)
+    # edge samples: every {0, 1, 127, 128, 254, 255}^3 triple, the greys, and
+    # triples whose weighted sum ends in exactly 500 (round half up)
+    levels = [0, 1, 127, 128, 254, 255]
+    samples = [(r, g, b) for r in levels for g in levels for b in levels]
+    samples += [(v, v, v) for v in range(256)]
+    half = []
+    for r in range(0, 256, 3):
+        for g in range(0, 256, 5):
+            for b in range(256):
+                if (299 * r + 587 * g + 114 * b) % 1000 == 500:
+                    half.append((r, g, b))
+                    break
+    samples += half
+    samples += [tuple(int(c) for c in t) for t in rng.integers(0, 256, (4000, 3))]
+    samples = np.array(samples, np.uint8)
+    n = len(samples)
+    p6 = b"P6\n%d 1\n255\n" % n + samples.tobytes()
+    sample_gray = ref.read_pnm(p6)[0]
+    img = rng.integers(0, 256, (40, 48, 3), dtype=np.uint8)
+    img[10:30, 12:40] = (200, 40, 90)  # a region, so the curve has structure
+    gray = ref.read_pnm(b"P6\n48 40\n255\n" + img.tobytes())
+    small = img[:5, :7]
+    p3 = ("P3\n7 5\n255\n" + " ".join(str(int(v)) for v in small.ravel()) + "\n").encode()
+    gray_p3 = ref.read_pnm(p3)
+    r = ref.analyze(gray, k=6, workers=2)
+    np.savez_compressed(os.path.join(HERE, "luma.npz"), samples=samples, sample_gray=sample_gray,
+                        rgb=img, gray=gray, gray_p3=gray_p3, sums=r["sum"], cards=r["card"],
+                        t0=np.int32(r["t0"]), topk=np.array(r["topk"], np.int32))
+    print(f"wrote {n} luma samples and a 48x40 RGB image (reference read_pnm)")
+
+
 def main():
     ref = oracle.Reference()
+    if "--luma-only" in sys.argv:
+        luma_golden(ref)
+        return
+    luma_golden(ref)
     imgs = corpus()
     shapes = np.array([im.shape for im in imgs], np.int32)
     flat = np.concatenate([im.ravel() for im in imgs]).astype(np.uint8)

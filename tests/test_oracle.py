@@ -146,3 +146,21 @@ def test_selection_golden(orc, selection):
             st, tk = orc.top_k(v, d, k)
             assert st == z["status"][i, k - 1]
             assert tk == [int(t) for t in z["topk"][i, k - 1] if t >= 0]
+
+
+def test_luma_oracle_against_reference_read_pnm(orc):
+    """Colour ingest: the oracle's luma601 restatement against the reference's
+    own read_pnm decoding of P6 / P3 streams (tests/golden/luma.npz)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "luma.npz"))
+    s = g["samples"]
+    assert np.array_equal(orc.rgb_to_gray(s[None]), g["sample_gray"][None])
+    assert np.array_equal(orc.rgb_to_gray(g["rgb"]), g["gray"])
+    assert np.array_equal(orc.rgb_to_gray(g["rgb"][:5, :7]), g["gray_p3"])
+    # the closed form (what the GPU kernel computes), on every sample
+    s64 = s.astype(np.int64)
+    t = 299 * s64[:, 0] + 587 * s64[:, 1] + 114 * s64[:, 2] + 500
+    assert np.array_equal(np.minimum(t // 1000, 255).astype(np.uint8), g["sample_gray"])
+    r = orc.analyze(g["gray"], 6)
+    assert np.array_equal(r["sum"], g["sums"]) and np.array_equal(r["card"], g["cards"])
+    assert r["t0"] == int(g["t0"]) and r["topk"] == list(g["topk"])

@@ -17,6 +17,9 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--depth", type=int, default=1, help="kohler_cuda_set_pipeline_depth")
+ap.add_argument("--rgb", action="store_true",
+                help="colour ingest: time the pipeline on an RGB version of the config "
+                     "(channels: the grey map shifted by 3 px, itself, its negative)")
 ap.add_argument("--segment", type=int, default=-1,
                 help=">= 0: time the segmentation pipeline instead (0: curve -> {t0} -> "
                      "two-class quantize per image, bench.cpp:266-281; k: top-k quantize)")
@@ -39,7 +42,12 @@ out = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
        "topk": torch.zeros((n, k), dtype=torch.int32, device="cuda"),
        "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda"),
        "status": torch.zeros(n, dtype=torch.int32, device="cuda")}
-if a.segment >= 0:
+if a.rgb:
+    xr = torch.stack([torch.roll(x, 3, dims=-1), x, 255 - x], dim=-1).contiguous()
+
+    def call(i):
+        ctx.analyze_rgb_batch_device(xr[i % copies], w, h, 3 * w, 3 * w * h, n, k, out)
+elif a.segment >= 0:
     kk = max(a.segment, 1)
     seg_out = torch.empty((n, h, w), dtype=torch.uint8, device="cuda")
     seg_ts = torch.zeros((n, kk), dtype=torch.int32, device="cuda")
@@ -64,7 +72,7 @@ if a.time:
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
     px = n * h * w
-    print(json.dumps({"config": a.config, "depth": a.depth, "segment": a.segment, "n": n, "w": w, "h": h,
+    print(json.dumps({"config": a.config, "rgb": a.rgb, "depth": a.depth, "segment": a.segment, "n": n, "w": w, "h": h,
                       "ms_per_step": ms,
                       "gpix_per_s": px / ms / 1e6, "hbm_frac": px / ms / 1e6 / 6452.8,
                       "images_per_s": n / ms * 1e3, "copies": copies, "steps": steps}))
