@@ -665,6 +665,10 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             // all lanes' copies into slot q & 3 are visible, and all lanes have
             // read slot (q - 1) & 3 (the previous position), which is refilled now
             __syncwarp();
+            // read this position's row first: the prefetch issue below
+            // covers the LDS latency before the unpack needs the data
+            Row r;
+            read_row(r, seg0 + (q & 3u) * kSlotBytes, offl, offr);
             const uint32_t pref = seg0 + ((q + 3u) & 3u) * kSlotBytes;
             if (!CROSS || j + 3 < P)
                 fetch_row(G, r0 + j + 3, pitch, pref);
@@ -672,8 +676,6 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 fetch_row(N, j + 3 - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
-            Row r;
-            read_row(r, seg0 + (q & 3u) * kSlotBytes, offl, offr);
             absorb<ALIGNED>(D, r, lane4, G.e);
             if (KIND == 1) {
                 // prime: q(up -> row r0) from row r0 - 1 (neutral at the band's first row)
@@ -972,6 +974,8 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
             const uint32_t q = pos + (uint32_t)j;
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             __syncwarp();
+            Row r;  // read first: the prefetch issue covers the LDS latency
+            read_row(r, seg0 + (q & 3u) * Lay::kSlot, offl, offr);
             const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
             if (!CROSS || j + 3 < P)
                 fetch_row(G, j + 3, pitch, pref);
@@ -979,8 +983,6 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
                 fetch_row(N, j + 3 - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
-            Row r;
-            read_row(r, seg0 + (q & 3u) * Lay::kSlot, offl, offr);
             absorb<ALIGNED>(D, r, lane4, G.e);
             if (KIND == 1) {
                 const bool has_up = G.y0 > 0;

@@ -1,4 +1,10 @@
-for c in C1 C3 C4 C5; do echo "new $(timeout 120 python tools/run_config.py --config $c --time 2>&1 | tail -1 | cut -c1-140)"; done
-cp paper_1707_05062_b200/lib/libkohler_cuda.so /tmp/new.so; cp ab_old/libkohler_cuda.so paper_1707_05062_b200/lib/libkohler_cuda.so
-for c in C1 C3 C4 C5; do echo "old $(timeout 120 python tools/run_config.py --config $c --time 2>&1 | tail -1 | cut -c1-140)"; done
+# A/B timing of the working-tree library against ab_old/libkohler_cuda.so
+# (built from the previous commit); same box, interleaved.
+set -u
+run() { for c in C2 C3 C4 C5; do d=1; [ $c = C2 ] && d=2; echo "$1 $(timeout 120 python tools/run_config.py --config $c --time --depth $d 2>&1 | tail -1 | cut -c1-150)"; done; }
+cp paper_1707_05062_b200/lib/libkohler_cuda.so /tmp/new.so
+for rep in 1 2; do
+  cp /tmp/new.so paper_1707_05062_b200/lib/libkohler_cuda.so; run new
+  cp ab_old/libkohler_cuda.so paper_1707_05062_b200/lib/libkohler_cuda.so; run old
+done
 cp /tmp/new.so paper_1707_05062_b200/lib/libkohler_cuda.so
