@@ -76,8 +76,10 @@ struct WideParams {
 #ifndef KOHLER_WALK_THREADS
 #define KOHLER_WALK_THREADS 384
 #endif
-constexpr int kWalkThreads = KOHLER_WALK_THREADS;
+constexpr int kWalkThreads = KOHLER_WALK_THREADS;  // K1
 constexpr int kWalkWarps = kWalkThreads / 32;
+constexpr int kTwThreads = 512;                     // K5 (its round layout assumes 16 warps)
+constexpr int kTwWarps = kTwThreads / 32;
 
 // Shared-memory map of K1 (dynamic), after the striped counters and corr
 // (kohler_walk.cuh).
@@ -86,7 +88,7 @@ constexpr int kWalkWarps = kWalkThreads / 32;
 // counter address is "register + compile-time immediate" (no base register
 // in the hot loop); everything else lives in the gap below it, at offsets
 // from the dynamic base.
-constexpr uint32_t kHistAbs = 0x10000;
+constexpr uint32_t kHistAbs = kWalkWarps > 16 ? 0x12000 : 0x10000;  // above the ring + scratch
 // Row ring of the column walks (cp.async destination): per warp kRingSlots
 // slots of 32 lane segments + a 16-byte pad on each side.  Idle during the
 // flush, so the reconstruction / selection scratch aliases it.
@@ -528,6 +530,44 @@ __device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitc
         : "memory");
 }
 
+// Steady-state prefetch of a segment (positions >= 3: no top clamp): the
+// lane's source row pointer advances by one pitch per position until the
+// walk reaches the buffer's last row (then it re-reads it).  The pad copies
+// of lanes 0 / 31 use immediate offsets (left pad: slot + 512 <- src - 16,
+// right pad: slot + 528 = lane 31's segment + 32 <- src + 16).
+struct FetchStream {
+    const uint8_t* src;
+    int left;     // positions the pointer may still advance
+    uint32_t pl;  // lane 0 with a left neighbour
+    uint32_t pr;  // lane 31 with a right neighbour
+};
+
+__device__ __forceinline__ FetchStream fetch_stream(const LaneGeo& L, int j, uint32_t pitch,
+                                                    int lane)
+{
+    FetchStream f;
+    const int jj = min(j, L.jcl);  // j >= 3 > jlo
+    f.src = L.p + (size_t)((uint32_t)jj * pitch);
+    f.left = L.jcl - j;
+    f.pl = L.pad && lane == 0;
+    f.pr = L.pad && lane == 31;
+    return f;
+}
+
+__device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint32_t dst)
+{
+    asm volatile(
+        "{\n\t.reg .pred pl, pr;\n\tsetp.ne.u32 pl, %2, 0;\n\tsetp.ne.u32 pr, %3, 0;\n\t"
+        "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
+        "@pl cp.async.cg.shared.global [%0+512], [%1+-16], 16;\n\t"
+        "@pr cp.async.cg.shared.global [%0+32], [%1+16], 16;\n\t"
+        "cp.async.commit_group;\n\t}" ::"r"(dst),
+        "l"(f.src), "r"(f.pl), "r"(f.pr)
+        : "memory");
+    f.src += f.left > 0 ? pitch : 0u;
+    --f.left;
+}
+
 // Read ring slot position of this lane back: the segment and its neighbour
 // bytes (a row start's left / a row end's right neighbour is the pixel
 // itself: equal => neutral; lanes next to each other in a warp are
@@ -636,10 +676,14 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         return;
 
     Car X, Y;
-    uint32_t pos = 0;  // ring position of the segment's position 0 (mod 4 picks the slot)
+    // ring slots of the current position and of the previous one (which the
+    // current step refills: (q + 3) & 3 == (q - 1) & 3)
+    const uint32_t slot_end = seg0 + kRingSlots * kSlotBytes;
+    uint32_t sl_cur = seg0, sl_prev = seg0 + (kRingSlots - 1) * kSlotBytes;
     for (;;) {
         const int L = r1 - r0;
         const int P = L + 2;
+        FetchStream fs = fetch_stream(G, r0 + 3, pitch, lane);
         const long long gn = g + 1;
         const bool has_next = gn * R < ub;
         const int nr1 = has_next ? (int)(ub - gn * R < (long long)R ? (int)(ub - gn * R) : R) : 0;
@@ -659,7 +703,6 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             constexpr bool CROSS = decltype(cross)::value;  // prefetch may cross into the next segment
             constexpr int WC = decltype(wc)::value;
             constexpr uint32_t kOffW = (WC && TWO_W) ? kOffW1 : kOffW0;
-            const uint32_t q = pos + (uint32_t)j;
             // slot q & 3 was committed 3 groups ago; <= 2 younger groups may pend
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             // all lanes' copies into slot q & 3 are visible, and all lanes have
@@ -668,10 +711,12 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             // read this position's row first: the prefetch issue below
             // covers the LDS latency before the unpack needs the data
             Row r;
-            read_row(r, seg0 + (q & 3u) * kSlotBytes, offl, offr);
-            const uint32_t pref = seg0 + ((q + 3u) & 3u) * kSlotBytes;
+            read_row(r, sl_cur, offl, offr);
+            const uint32_t pref = sl_prev;
+            sl_prev = sl_cur;
+            sl_cur = sl_cur + kSlotBytes == slot_end ? seg0 : sl_cur + kSlotBytes;
             if (!CROSS || j + 3 < P)
-                fetch_row(G, r0 + j + 3, pitch, pref);
+                fetch_next(fs, pitch, pref);
             else if (has_next)
                 fetch_row(N, j + 3 - P, pitch, pref);
             else
@@ -755,7 +800,6 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             step(X, Y, j, K2{}, W0{}, CR{});
         if (!has_next)
             break;
-        pos += (uint32_t)P;
         g = gn;
         r0 = 0;
         r1 = nr1;
@@ -879,7 +923,7 @@ struct TwLayout {
     // 32 lane segments (512 B, 128-byte aligned), then 2 pads per group
     static constexpr uint32_t kSlot = (512 + 32 * NG + 127) / 128 * 128;
     static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
-    static constexpr uint32_t kRingBytes = kWalkWarps * kRingSlots * kSlot + 128;
+    static constexpr uint32_t kRingBytes = kTwWarps * kRingSlots * kSlot + 128;
     static constexpr uint32_t kCorr = kRingBytes;  // int[NG][256]
     static constexpr uint32_t kEnd = kCorr + NG * 1024;
     static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
@@ -910,7 +954,7 @@ __device__ __forceinline__ LaneGeo tw_geo(const TwParams& p, long long img, int 
 }
 
 template <bool ALIGNED, int LG>
-__global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p)
+__global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
 {
     using namespace kohler_walk;
     using Lay = TwLayout<LG>;
@@ -950,9 +994,9 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
     fetch_row(G, 2, pitch, seg0 + 2 * Lay::kSlot);
     {
         uint4* z = reinterpret_cast<uint4*>(hist);
-        for (int i = tid; i < (int)(kHistBytes / 16); i += kWalkThreads)
+        for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
             z[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < NG * 256; i += kWalkThreads)
+        for (int i = tid; i < NG * 256; i += kTwThreads)
             reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
     }
     __syncthreads();
@@ -1085,11 +1129,11 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
             // 1. every thread: 2*NG (half-row, group) cells, contiguous 16-byte
             //    pieces across a warp (conflict free): read, sum the group's LG
             //    lane words (fields for W), clear
-            constexpr int PER = 1024 * NG / kWalkThreads;
+            constexpr int PER = 1024 * NG / kTwThreads;
             uint32_t va[PER], vb[PER];
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
-                const int idx = tid + kWalkThreads * q;
+                const int idx = tid + kTwThreads * q;
                 const int rh = idx / NG, gg = idx % NG;
                 uint32_t a = 0, b = 0;
 #pragma unroll
@@ -1114,7 +1158,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
             uint32_t* scr = reinterpret_cast<uint32_t*>(hist);
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
-                const int idx = tid + kWalkThreads * q;
+                const int idx = tid + kTwThreads * q;
                 const int rh = idx / NG, gg = idx % NG;
                 const int row = rh >> 1;
                 uint32_t* base = scr + gg * kTwImgWords;
@@ -1169,9 +1213,9 @@ __global__ void __launch_bounds__(kWalkThreads, 1) twalk_kernel(const TwParams p
             __syncthreads();
             // 4. clear the scratch and the border terms for the next round
             uint4* z = reinterpret_cast<uint4*>(hist);
-            for (int i = tid; i < NG * kTwImgWords / 4; i += kWalkThreads)
+            for (int i = tid; i < NG * kTwImgWords / 4; i += kTwThreads)
                 z[i] = make_uint4(0, 0, 0, 0);
-            for (int i = tid; i < NG * 256; i += kWalkThreads)
+            for (int i = tid; i < NG * 256; i += kTwThreads)
                 reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
         __syncthreads();
@@ -2094,7 +2138,7 @@ int launch_twalk_t(const TwParams& tp, unsigned G, cudaStream_t stream)
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         attr_set = true;
     }
-    KC_CUDA(launch_pdl(twalk_kernel<ALIGNED, LG>, G, kWalkThreads, kSmWideBytes, stream, tp));
+    KC_CUDA(launch_pdl(twalk_kernel<ALIGNED, LG>, G, kTwThreads, kSmWideBytes, stream, tp));
     return KOHLER_OK;
 }
 
@@ -2108,7 +2152,7 @@ bool twalk_geometry(int n, int w, int h, int& lg, int& R, int& C)
     for (int cand = 4; cand <= 32; cand *= 2) {
         if (32 / cand > n && cand < 32)
             continue;  // fewer images than groups: use bigger groups
-        const int walkers = kWalkWarps * cand;
+        const int walkers = kTwWarps * cand;
         if (S > walkers)
             continue;
         const int c = walkers / S;
