@@ -151,6 +151,10 @@ def cpu_reference_time(img: np.ndarray, budget_s: float, max_runs: int):
     return med, runs, cores, ref.active_kernel()
 
 
+def workload_name(w: int, h: int) -> str:
+    return f"{CONFIG_NAME} {w}x{h} gradient+40 ellipses+N(0,5^2), seed 0x51C2, k={K_TOP}"
+
+
 def run_reference(args, rank: int, world: int):
     """--impl reference: the reference's CPU implementation on this host."""
     if rank != 0:
@@ -173,7 +177,7 @@ def run_reference(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": f"{CONFIG_NAME} {w}x{h} gradient+ellipses+N(0,5^2), k={K_TOP}",
+        "config": {"workload": workload_name(w, h),
                    "parallelism": f"{cores} host threads (reference fast_contrast_curve workers)"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"full {CONFIG_NAME} image per step, kernel={ref.active_kernel()}"},
@@ -345,8 +349,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": f"{CONFIG_NAME} {w}x{h} gradient+40 ellipses+N(0,5^2), seed "
-                                   f"0x51C2, k={K_TOP}",
+            "config": {"workload": workload_name(w, h),
                        "parallelism": parallel,
                        "l2": f"rotating {copies} input copies ({copies * buf[0].numel() / 1e6:.0f} MB"
                              f" > 2x L2 {l2 / 1e6:.0f} MB)",
