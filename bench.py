@@ -198,20 +198,24 @@ def main():
     ap.add_argument("--depth", type=int, default=2,
                     help="K1 launches in flight for the device-resident step loop "
                          "(kohler_cuda_set_pipeline_depth; 1 = each launch on all SMs)")
+    ap.add_argument("--force-bands", action="store_true",
+                    help="run the multi-GPU row-band path (NCCL) even at N=1 (launch under "
+                         "torchrun; exercises the N>1 code on one GPU, not a scaling number)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    bands = world > 1 or (args.force_bands and args.impl == "ours")
+    if world > 1 or bands:
         if args.impl == "ours":
             torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
 
     if args.impl == "reference":
         run_reference(args, rank, world)
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
 
@@ -225,7 +229,7 @@ def main():
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     stream = torch.cuda.current_stream()
 
-    if world == 1:
+    if not bands:
         pitch = (w + 127) // 128 * 128
         img_bytes = pitch * h
         copies = max(2, (2 * l2) // img_bytes + 1)
@@ -261,13 +265,21 @@ def main():
         out = ba.out
 
         def step(i):
-            ba.step(buf[i % copies], pitch)
+            # all-reduce of step i overlapped with step i + 1's band K1; the
+            # selection of step i runs behind it (drain() after the last step)
+            ba.step_pipelined(i, buf[i % copies], pitch)
         launches_per_step = 2
         bytes_per_step = w * h  # whole job processes the full image per step
-        parallel = f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64, strong scaling"
+        parallel = (f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64 overlapped with "
+                    "the next step's band kernel, strong scaling")
+
+    def drain():
+        if bands:
+            ba.drain()
 
     # correctness gate before timing (bench.cpp:141-161 semantics)
     step(0)
+    drain()
     torch.cuda.synchronize()
     if launches_per_step is None:
         launches_per_step = ctx.last_launch_count()
@@ -277,7 +289,7 @@ def main():
         got_t0 = int(out["t0"][0])
         got_tk = out["topk"][: int(out["topk_count"][0])].tolist()
         ok = got_t0 == exp["t0"] and got_tk == exp["topk"]
-        if world == 1:
+        if not bands:
             ok = ok and np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"]) \
                 and np.array_equal(out["cards"].cpu().numpy().view(np.uint64), exp["card"])
         if not ok:
@@ -285,6 +297,7 @@ def main():
 
     for i in range(args.warmup):
         step(i)
+    drain()
     torch.cuda.synchronize()
 
     sampler = ClockSampler(dev.index if world == 1 else local).start()
@@ -297,6 +310,7 @@ def main():
     e0.record(stream)
     for i in range(args.steps):
         step(i)
+    drain()  # the last step's selection is inside the timed region
     e1.record(stream)
     e1.synchronize()
     if world > 1:
@@ -313,7 +327,7 @@ def main():
 
     # kernel-level timing of K1 alone (its own events, same stream), for the roofline
     kern_ms = None
-    if world == 1:
+    if not bands:
         # one K1 launch per step: with d launches in flight the step time is
         # K1's effective (throughput) time per launch
         kern_ms = ms_step
@@ -330,16 +344,28 @@ def main():
         k1.synchronize()
         kern_ms = k0.elapsed_time(k1) / nk
     peak, peak_src = peaks()
-    kbytes = w * h if world == 1 else (ba.r1 - ba.r0) * w
+    kbytes = w * h if not bands else (ba.r1 - ba.r0) * w
     achieved = kbytes / (kern_ms * 1e-3) / 1e9
+
+    # N > 1: every rank uploads its band (own rows + halo) from pinned host
+    # memory each step, runs K1 on it, all-reduces, selects and reads the
+    # thresholds back; wall clock, max over ranks
+    e2e_bands = None
+    if bands:
+        try:
+            e2e_bands = measure_e2e_bands(ba, img, args, dev, pitch)
+        except Exception as exc:  # keep the device-timed line
+            e2e_bands = {"error": f"{type(exc).__name__}: {exc}"}
 
     line = None
     if rank == 0:
         e2e = None
         cpu = None
-        if world == 1:
+        if not bands:
             ctx.set_pipeline_depth(1)  # the host API call is measured one call at a time
             e2e = measure_e2e(ctx, img, args)
+        else:
+            e2e = e2e_bands
             med, runs, cores, kern = cpu_reference_time(img.numpy(), args.cpu_budget, 2000)
             cpu = {"value": w * h / med / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": f"full {CONFIG_NAME} image, median of {runs} runs (1 warm-up), "
@@ -354,10 +380,10 @@ def main():
                        "l2": f"rotating {copies} input copies ({copies * buf[0].numel() / 1e6:.0f} MB"
                              f" > 2x L2 {l2 / 1e6:.0f} MB)",
                        "launch": "eager",
-                       "pipeline_depth": args.depth if world == 1 else 1},
+                       "pipeline_depth": args.depth if not bands else 1},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "walk_kernel<true> (K1; finish_kernel K3/K4 PDL-overlapped)" if world == 1
+                         "kernel": "walk_kernel<true> (K1; finish_kernel K3/K4 PDL-overlapped)" if not bands
                          else "walk_kernel<true> band partial (K1)",
                          "algorithmic_bytes_per_launch": kbytes, "kernel_ms": kern_ms,
                          "peak_source": peak_src},
@@ -367,9 +393,47 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_e2e_bands(ba, img, args, dev, pitch):
+    """e2e at N > 1 through the band API: pinned host rows of this rank's
+    band -> H2D -> K1 band partial -> NCCL all-reduce -> device selection ->
+    D2H of t0 / top-k, every step; wall clock per rank, max over ranks."""
+    h, w = img.shape
+    rows = max(ba.rows_held, 1)
+    host = torch.zeros((rows, pitch), dtype=torch.uint8).pin_memory()
+    if ba.rows_held:
+        host[:, :w] = img[ba.lo:ba.hi]
+    dbuf = torch.empty((rows, pitch), dtype=torch.uint8, device=dev)
+    res = torch.zeros(2 + K_TOP, dtype=torch.int32).pin_memory()
+    n = args.e2e_steps or min(args.steps, 200)
+
+    def call():
+        dbuf.copy_(host, non_blocking=True)
+        ba.step(dbuf, pitch)
+        res[0:1].copy_(ba.out["t0"], non_blocking=True)
+        res[1:2].copy_(ba.out["topk_count"], non_blocking=True)
+        res[2:].copy_(ba.out["topk"], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    for _ in range(3):
+        call()
+    dist.barrier()
+    st = time.perf_counter()
+    for _ in range(n):
+        call()
+    el = time.perf_counter() - st
+    t = torch.tensor([el, float(rows * pitch), 4.0 * (2 + K_TOP)], dtype=torch.float64, device=dev)
+    tb = t.clone()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+    el = float(t[0].item())
+    return {"value": w * h * n / el / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": int(tb[1].item()), "d2h_bytes_per_step": int(tb[2].item()),
+            "steps": n, "path": "per rank: pinned band rows -> H2D -> band K1 -> NCCL all-reduce "
+                                "-> select -> D2H, wall clock, max over ranks"}
 
 
 def measure_e2e(ctx, img, args):

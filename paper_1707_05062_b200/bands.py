@@ -36,12 +36,17 @@ class BandedAnalyzer:
     """Per-rank driver: partial curve of the rank's band (K1 on the GPU),
     NCCL all-reduce of the 512 u64 partials, device selection (K4)."""
 
-    def __init__(self, ctx, w: int, h: int, world: int, rank: int, k: int = 6, group=None):
+    def __init__(self, ctx, w: int, h: int, world: int, rank: int, k: int = 6, group=None,
+                 device=None):
         self.ctx, self.w, self.h, self.k, self.group = ctx, w, h, k, group
         self.r0, self.r1 = band_bounds(h, world, rank)
         self.lo, self.hi = band_slice(h, self.r0, self.r1)
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.curve = torch.zeros(512, dtype=torch.int64, device=dev)
+        # pipelined steps: two partial buffers, the all-reduce of step i in
+        # flight while step i + 1's band accumulates
+        self._curves = [torch.zeros(512, dtype=torch.int64, device=dev) for _ in range(2)]
+        self._pending = None  # (work handle, buffer) of the previous step
         self.out = {"values": torch.zeros(256, dtype=torch.float64, device=dev),
                     "defined": torch.zeros(256, dtype=torch.uint8, device=dev),
                     "t0": torch.zeros(1, dtype=torch.int32, device=dev),
@@ -53,6 +58,38 @@ class BandedAnalyzer:
     def rows_held(self) -> int:
         return self.hi - self.lo
 
+    def _select(self, curve: torch.Tensor) -> None:
+        self.ctx.select_device(curve.data_ptr(), curve.data_ptr() + 256 * 8, 1, 256, self.k,
+                               self.out)
+
+    def step_pipelined(self, i: int, band: torch.Tensor, pitch: int) -> None:
+        """Step i with the all-reduce overlapped: K1 of this band into buffer
+        i % 2, an asynchronous all-reduce of it (NCCL's stream, after K1),
+        then -- on the compute stream, behind this K1 -- the selection of the
+        PREVIOUS step's merged curve.  ``drain()`` completes the last step.
+        Every step's result is the same as ``step``'s; ``out`` holds step
+        i - 1's selection after this call (step i's after ``drain``)."""
+        cur = self._curves[i % 2]
+        if self.r1 > self.r0:
+            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
+                                       cur.data_ptr(), cur.data_ptr() + 256 * 8)
+        else:
+            cur.zero_()
+        work = None
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            work = dist.all_reduce(cur, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.drain()
+        self._pending = (work, cur)
+
+    def drain(self) -> None:
+        if self._pending is None:
+            return
+        work, buf = self._pending
+        if work is not None:
+            work.wait()  # the compute stream waits for the all-reduce
+        self._select(buf)
+        self._pending = None
+
     def step(self, band: torch.Tensor, pitch: int) -> None:
         """band: CUDA uint8 buffer holding rows [lo, hi) with row pitch `pitch`."""
         if self.r1 > self.r0:
@@ -61,5 +98,4 @@ class BandedAnalyzer:
         else:
             self.curve.zero_()
         allreduce_curve(self.curve, self.group)
-        self.ctx.select_device(self.curve.data_ptr(), self.curve.data_ptr() + 256 * 8, 1, 256,
-                               self.k, self.out)
+        self._select(self.curve)

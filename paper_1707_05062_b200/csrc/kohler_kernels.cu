@@ -1298,6 +1298,9 @@ struct SelectParams {
 __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
 {
     extern __shared__ __align__(16) unsigned char sm[];
+    // the next launch may start at once: every kernel that reads this one's
+    // outputs executes griddepcontrol.wait before it does
+    pdl_trigger();
     pdl_wait();  // curves may come from the preceding (PDL-overlapped) launch
     const int n = p.levels;
     const int cidx = blockIdx.x;
@@ -1344,6 +1347,9 @@ __global__ void __launch_bounds__(256) select256_kernel(const SelectParams p)
 {
     __shared__ double smv[8][128];
     __shared__ int smt[8][128];
+    // the next launch may start at once: every kernel that reads this one's
+    // outputs executes griddepcontrol.wait before it does
+    pdl_trigger();
     pdl_wait();  // curves may come from the preceding (PDL-overlapped) launch
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const long long cidx = (long long)blockIdx.x * 8 + wq;

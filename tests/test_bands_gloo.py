@@ -79,3 +79,82 @@ def test_gloo_band_merge_is_exact(orc, world):
     for _, buf in got:
         assert np.array_equal(buf[:256].view(np.uint64), s)
         assert np.array_equal(buf[256:].view(np.uint64), c)
+
+
+class _OracleCtx:
+    """Stands in for the CUDA context on CPU: the band partial and the
+    selection come from the oracle, written through the same raw pointers
+    the C ABI receives."""
+
+    def __init__(self, orc, img):
+        self.orc, self.img = orc, img
+
+    def band_curve_device(self, band, w, pitch, h_total, r0, r1, sum_ptr, card_ptr, stream=None):
+        import ctypes
+        local = np.ascontiguousarray(self.img[r0:min(r1 + 1, h_total)])
+        s, c = self.orc.curve_rows(local, 0, r1 - r0)
+        ctypes.memmove(sum_ptr, s.ctypes.data, 2048)
+        ctypes.memmove(card_ptr, c.ctypes.data, 2048)
+
+    def select_device(self, sums, cards, n, levels, k, out, stream=None):
+        import ctypes
+        s = np.zeros(256, np.uint64)
+        c = np.zeros(256, np.uint64)
+        ctypes.memmove(s.ctypes.data, sums, 2048)
+        ctypes.memmove(c.ctypes.data, cards, 2048)
+        v, d = self.orc.mean_contrast(s, c)
+        st, ts = self.orc.top_k(v, d, k)
+        out["t0"][0] = self.orc.optimal_threshold(v, d)
+        out["topk_count"][0] = len(ts)
+        out["topk"][: len(ts)] = torch.tensor(ts, dtype=torch.int32)
+        out["status"][0] = st
+
+
+def _worker_pipelined(rank, world, port, imgs, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1707_05062_b200.bands import BandedAnalyzer
+    orc = oracle.Oracle()
+    h, w = imgs[0].shape
+    ctx = _OracleCtx(orc, imgs[0])
+    ba = BandedAnalyzer(ctx, w, h, world, rank, k, device=torch.device("cpu"))
+    got = []
+    for i, im in enumerate(imgs):
+        ctx.img = im  # the band K1 of step i sees image i
+        ba.step_pipelined(i, None, w)
+        if i > 0:  # out now holds step i - 1
+            got.append((int(ba.out["t0"][0]), ba.out["topk"][: int(ba.out["topk_count"][0])].tolist()))
+    ba.drain()
+    got.append((int(ba.out["t0"][0]), ba.out["topk"][: int(ba.out["topk_count"][0])].tolist()))
+    q.put((rank, got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_pipelined_steps(orc, world):
+    """The overlapped schedule of bench.py at N > 1 (async all-reduce of step
+    i while step i + 1 accumulates, selection one step behind, drain at the
+    end) yields every step's exact thresholds."""
+    rng = np.random.default_rng(100 + world)
+    imgs = []
+    for i in range(5):
+        a = rng.integers(0, 256, (41, 29), dtype=np.uint8)
+        a[5 + i:20 + i] = rng.integers(0, 256)
+        imgs.append(a)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_pipelined, args=(r, world, port, imgs, 6, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [(e["t0"], e["topk"]) for e in (orc.analyze(im, 6) for im in imgs)]
+    for _, got in res:
+        assert got == want
