@@ -58,9 +58,49 @@ class BandedAnalyzer:
     def rows_held(self) -> int:
         return self.hi - self.lo
 
+    def _fast_calls(self):
+        """Raw C-ABI calls with the pointers resolved once: the per-step host
+        cost (ctypes + tensor pointer lookups) otherwise exceeds the device
+        time of a small band.  Only for a real CUDA context on the current
+        stream (the CPU tests pass a stand-in context)."""
+        lib = getattr(self.ctx, "_lib", None)
+        if lib is None:
+            return None
+        if getattr(self, "_fc", None) is None:
+            o = self.out
+            st = torch.cuda.current_stream().cuda_stream
+            h = self.ctx.handle
+            outs = (o["values"].data_ptr(), o["defined"].data_ptr(), o["t0"].data_ptr(),
+                    o["topk"].data_ptr(), o["topk_count"].data_ptr(), o["status"].data_ptr())
+            self._fc = (lib, h, st, outs)
+        return self._fc
+
     def _select(self, curve: torch.Tensor) -> None:
-        self.ctx.select_device(curve.data_ptr(), curve.data_ptr() + 256 * 8, 1, 256, self.k,
-                               self.out)
+        fc = self._fast_calls()
+        if fc is None:
+            self.ctx.select_device(curve.data_ptr(), curve.data_ptr() + 256 * 8, 1, 256, self.k,
+                                   self.out)
+            return
+        lib, h, st, outs = fc
+        p = curve.data_ptr()
+        rc = lib.kohler_cuda_select_device(h, p, p + 2048, 1, 256, self.k, *outs, st)
+        if rc:
+            from .api import _raise_for
+            _raise_for(rc)
+
+    def _band(self, band, pitch: int, cur: torch.Tensor) -> None:
+        fc = self._fast_calls()
+        if fc is None:
+            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
+                                       cur.data_ptr(), cur.data_ptr() + 256 * 8)
+            return
+        lib, h, st, _ = fc
+        p = cur.data_ptr()
+        rc = lib.kohler_cuda_band_curve_device(h, band.data_ptr(), self.w, pitch, self.h, self.r0,
+                                               self.r1, p, p + 2048, st)
+        if rc:
+            from .api import _raise_for
+            _raise_for(rc)
 
     def step_pipelined(self, i: int, band: torch.Tensor, pitch: int) -> None:
         """Step i with the all-reduce overlapped: K1 of this band into buffer
@@ -71,8 +111,7 @@ class BandedAnalyzer:
         i - 1's selection after this call (step i's after ``drain``)."""
         cur = self._curves[i % 2]
         if self.r1 > self.r0:
-            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
-                                       cur.data_ptr(), cur.data_ptr() + 256 * 8)
+            self._band(band, pitch, cur)
         else:
             cur.zero_()
         work = None
@@ -93,8 +132,7 @@ class BandedAnalyzer:
     def step(self, band: torch.Tensor, pitch: int) -> None:
         """band: CUDA uint8 buffer holding rows [lo, hi) with row pitch `pitch`."""
         if self.r1 > self.r0:
-            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
-                                       self.curve.data_ptr(), self.curve.data_ptr() + 256 * 8)
+            self._band(band, pitch, self.curve)
         else:
             self.curve.zero_()
         allreduce_curve(self.curve, self.group)
