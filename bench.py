@@ -198,6 +198,9 @@ def main():
     ap.add_argument("--depth", type=int, default=2,
                     help="K1 launches in flight for the device-resident step loop "
                          "(kohler_cuda_set_pipeline_depth; 1 = each launch on all SMs)")
+    ap.add_argument("--graph-steps", type=int, default=60,
+                    help="N=1: replay the step loop from CUDA graphs of this many consecutive "
+                         "steps (PDL edges between them inside the graph); 0 = eager launches")
     ap.add_argument("--force-bands", action="store_true",
                     help="run the multi-GPU row-band path (NCCL) even at N=1 (launch under "
                          "torchrun; exercises the N>1 code on one GPU, not a scaling number)")
@@ -246,8 +249,8 @@ def main():
 
         ctx.set_pipeline_depth(args.depth)
 
-        def step(i):
-            ctx.analyze_batch_device(buf[i % copies], w, h, pitch, img_bytes, 1, K_TOP, out, stream)
+        def step(i, st=stream):
+            ctx.analyze_batch_device(buf[i % copies], w, h, pitch, img_bytes, 1, K_TOP, out, st)
         launches_per_step = None  # counted after the first step (K1 walk + K3/K4 finish)
         bytes_per_step = w * h
         parallel = ("1 GPU, K1 walk + K3/K4 finish per step (PDL-chained)"
@@ -300,6 +303,21 @@ def main():
     drain()
     torch.cuda.synchronize()
 
+    # N=1: a step is one K1 + one finish launch (~9-15 us of host API time per
+    # step through ctypes, as long as the device step): replay the loop from
+    # CUDA graphs of G consecutive steps, captured through the same public
+    # device API on the capture stream (PDL edges between the steps inside)
+    graph = None
+    G = args.graph_steps if not bands else 0
+    if G > 0:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            cap = torch.cuda.current_stream()
+            for j in range(G):
+                step(j, cap)
+        graph.replay()
+        torch.cuda.synchronize()
+
     sampler = ClockSampler(dev.index if world == 1 else local).start()
     sampler.wait_first()
     if world > 1:
@@ -308,7 +326,13 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for i in range(args.steps):
+    i = 0
+    if graph is not None:
+        with torch.cuda.stream(stream):
+            while i + G <= args.steps:
+                graph.replay()
+                i += G
+    for i in range(i, args.steps):
         step(i)
     drain()  # the last step's selection is inside the timed region
     e1.record(stream)
@@ -317,6 +341,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    if rank == 0 and not bands:
+        # the replayed / pipelined steps left the last image's full result
+        ok = int(out["t0"][0]) == exp["t0"] and \
+            out["topk"][: int(out["topk_count"][0])].tolist() == exp["topk"] and \
+            np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"])
+        if not ok:
+            raise SystemExit("timed steps produced a result that differs from the oracle")
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -379,7 +410,9 @@ def main():
                        "parallelism": parallel,
                        "l2": f"rotating {copies} input copies ({copies * buf[0].numel() / 1e6:.0f} MB"
                              f" > 2x L2 {l2 / 1e6:.0f} MB)",
-                       "launch": "eager",
+                       "launch": (f"CUDA-graph replay, {G} steps per graph (PDL edges inside), "
+                                  "captured through kohler_cuda_analyze_batch_device"
+                                  if graph is not None else "eager"),
                        "pipeline_depth": args.depth if not bands else 1},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
