@@ -195,7 +195,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0,
                     help="seconds of CPU-baseline sampling (rank 0, N=1)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: min(steps, 200)")
-    ap.add_argument("--depth", type=int, default=2,
+    ap.add_argument("--depth", type=int, default=3,
                     help="K1 launches in flight for the device-resident step loop "
                          "(kohler_cuda_set_pipeline_depth; 1 = each launch on all SMs)")
     ap.add_argument("--graph-steps", type=int, default=60,
