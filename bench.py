@@ -470,9 +470,13 @@ def measure_e2e_bands(ba, img, args, dev, pitch):
 
 
 def measure_e2e(ctx, img, args):
-    """Same metric through the public host API (kohler_cuda_analyze via
-    Context.analyze_batch): pinned host image -> H2D -> fused kernel -> D2H
-    of curve + mean curve + thresholds, every step, wall-clocked."""
+    """Same metric through the public host C ABI, every step: the image from
+    pinned host memory -> H2D -> K1 + finish -> D2H of curve, mean curve and
+    thresholds.  Headline: the streaming API (kohler_cuda_submit /
+    kohler_cuda_collect, two steps in flight, so step i + 1's upload runs
+    under step i's kernels); also reported: the synchronous
+    kohler_cuda_analyze (one blocking call per step).  Wall clock, best of
+    three blocks of n steps each (a shared box's host / PCIe jitter)."""
     import ctypes as C
     h, w = img.shape
     pinned = torch.empty((h, w), dtype=torch.uint8).pin_memory()
@@ -484,37 +488,58 @@ def measure_e2e(ctx, img, args):
     t0 = np.zeros(1, np.int32)
     tk = np.zeros(K_TOP, np.int32)
     cnt = np.zeros(1, np.int32)
+    stt = np.zeros(1, np.int32)
     lib = ctx._lib
+    hd = ctx.handle
+    ptr = pinned.data_ptr()
+    outs = (res["s"].ctypes.data, res["c"].ctypes.data, vals.ctypes.data, dfn.ctypes.data,
+            t0.ctypes.data, tk.ctypes.data, cnt.ctypes.data, stt.ctypes.data)
+    ticket = C.c_longlong(-1)
 
-    def call():
-        return lib.kohler_cuda_analyze(ctx.handle, pinned.data_ptr(), w, h, w, K_TOP,
-                                       res["s"].ctypes.data, res["c"].ctypes.data,
-                                       vals.ctypes.data, dfn.ctypes.data, t0.ctypes.data,
-                                       tk.ctypes.data, cnt.ctypes.data)
-    for _ in range(3):
-        call()
-    # three blocks of n calls, the best block reported (host wall clock on a
-    # shared box picks up OS / PCIe jitter; every block is a full e2e run)
-    best = None
-    for _ in range(3):
-        per = []
-        st = time.perf_counter()
+    def sync_call():
+        return lib.kohler_cuda_analyze(hd, ptr, w, h, w, K_TOP, *outs[:7])
+
+    def submit():
+        if lib.kohler_cuda_submit(hd, ptr, 1, w, h, w, w * h, K_TOP, C.byref(ticket)):
+            raise RuntimeError("e2e submit failed")
+        return ticket.value
+
+    def collect(t):
+        if lib.kohler_cuda_collect(hd, t, *outs):
+            raise RuntimeError("e2e collect failed")
+
+    def stream_block():
+        prev = submit()
+        for _ in range(n - 1):
+            nxt = submit()
+            collect(prev)
+            prev = nxt
+        collect(prev)
+
+    def sync_block():
         for _ in range(n):
-            c0 = time.perf_counter()
-            rc = call()
-            per.append(time.perf_counter() - c0)
-            if rc not in (0, 1):
+            if sync_call() not in (0, 1):
                 raise RuntimeError("e2e call failed")
-        el = time.perf_counter() - st
-        if best is None or el < best[0]:
-            best = (el, sorted(per))
-    el, per = best
+
+    def best(block):
+        block()  # warm-up block
+        el = []
+        for _ in range(3):
+            st = time.perf_counter()
+            block()
+            el.append(time.perf_counter() - st)
+        return min(el)
+    el_sync = best(sync_block)
+    el = best(stream_block)
+    if int(t0[0]) < 0 or int(cnt[0]) < 1:
+        raise RuntimeError("e2e produced no thresholds")
     d2h = 256 * 8 * 2 + 256 * 8 + 256 + 4 * 3 + 4 * K_TOP
     return {"value": w * h * n / el / 1e9, "unit": UNIT, "h2d_bytes_per_step": w * h,
             "d2h_bytes_per_step": d2h, "steps": n,
-            "call_us": {"mean": el / n * 1e6, "median": per[n // 2] * 1e6, "min": per[0] * 1e6,
-                        "max": per[-1] * 1e6},
-            "path": "kohler_cuda_analyze (host API), pinned input, wall clock, best of 3 blocks"}
+            "call_us": el / n * 1e6,
+            "sync_value": w * h * n / el_sync / 1e9, "sync_call_us": el_sync / n * 1e6,
+            "path": "kohler_cuda_submit / kohler_cuda_collect (host C ABI, two steps in flight), "
+                    "pinned input, wall clock, best of 3 blocks; sync_* = kohler_cuda_analyze"}
 
 
 if __name__ == "__main__":

@@ -154,6 +154,24 @@ int kohler_cuda_last_launch_count(const kohler_cuda_ctx *ctx);
  * API's chunked uploads always use depth 1. */
 int kohler_cuda_set_pipeline_depth(kohler_cuda_ctx *ctx, int depth);
 
+/* ---- streaming host API (ABI 1.1) ----------------------------------------
+ * The per-image pipeline of kohler_cuda_analyze_batch, split so consecutive
+ * calls overlap: submit uploads the batch (host memory, pinned for full PCIe
+ * speed) on the copy stream and enqueues the kernels and the copy-back of the
+ * results; it returns at once with a ticket.  collect waits for that ticket
+ * and writes the outputs (any may be NULL; status[i] is 0 or
+ * KOHLER_NO_BOUNDARY per image).  At most two tickets are in flight: submit
+ * fails with KOHLER_INVALID_ARGUMENT until the ticket submitted two calls
+ * earlier has been collected.  With a stream of images, image i + 1's upload
+ * runs under image i's kernels and copy-back, so the loop is PCIe-bound
+ * (the reference's fast_contrast_curve has no counterpart; its callers'
+ * frame loops, e.g. bench_video (src/bench.cpp:264-284), are the users). */
+int kohler_cuda_submit(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w, int h, size_t pitch,
+                       size_t image_stride, int k, long long *ticket);
+int kohler_cuda_collect(kohler_cuda_ctx *ctx, long long ticket, uint64_t *sums, uint64_t *cards,
+                        double *values, uint8_t *defined, int *t0s, int *topks, int *topk_counts,
+                        int *status);
+
 /* ---- colour ingest (ABI 1.1) ------------------------------------------
  * Rec. 601 integer luma of interleaved 8-bit RGB, bit-identical to the
  * reference's luma601 (proj/src/pnm.cpp:63-68) that read_pnm applies to

@@ -53,6 +53,8 @@ SIGNATURES = {
     "kohler_cuda_last_launch_count": (_i, [_vp]),
     "kohler_cuda_set_pipeline_depth": (_i, [_vp, _i]),
     "kohler_cuda_rgb_to_gray": (_i, [_vp, _vp, _i, _i, _sz, _vp, _sz]),
+    "kohler_cuda_submit": (_i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp]),
+    "kohler_cuda_collect": (_i, [_vp, C.c_longlong, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kohler_cuda_rgb_to_gray_device": (_i, [_vp, _vp, _i, _i, _i, _sz, _sz, _vp, _sz, _sz, _vp]),
     "kohler_cuda_analyze_rgb_batch": (
         _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

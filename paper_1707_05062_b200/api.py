@@ -286,6 +286,38 @@ class Context:
             _stream(stream)))
 
 
+    # ---- streaming host API ---------------------------------------------------
+    def submit(self, px, k: int = 6) -> int:
+        """Enqueue the pipeline on host image(s) px[n, h, w] / [h, w] (u8; a
+        pinned torch tensor uploads at full PCIe speed) and return a ticket;
+        ``collect(ticket)`` returns the results.  Two tickets may be in flight,
+        so image i + 1's upload overlaps image i's kernels."""
+        if hasattr(px, "data_ptr"):  # torch CPU tensor (e.g. pinned)
+            t = px.contiguous()
+            n, h, w = (1, *t.shape) if t.dim() == 2 else tuple(t.shape)
+            ptr, keep = t.data_ptr(), t
+        else:
+            a = np.ascontiguousarray(px, dtype=np.uint8)
+            if a.ndim == 2:
+                a = a[None]
+            n, h, w = a.shape
+            ptr, keep = _ptr(a), a
+        tk = C.c_longlong(-1)
+        _raise_for(self._lib.kohler_cuda_submit(self._h, ptr, n, w, h, w, w * h, int(k),
+                                                C.byref(tk)))
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[tk.value] = (keep, n, int(k))
+        return tk.value
+
+    def collect(self, ticket: int) -> BatchResult:
+        keep, n, k = self._inflight.pop(ticket)
+        r = _alloc_result(n, k, True, True)
+        _raise_for(self._lib.kohler_cuda_collect(
+            self._h, int(ticket), _optr(r.sums), _optr(r.cards), _optr(r.values), _optr(r.defined),
+            _ptr(r.t0), _ptr(r.topk), _ptr(r.topk_count), _ptr(r.status)))
+        del keep
+        return r
+
     # ---- colour ingest (SURVEY.md §8f rank 3) ------------------------------
     def rgb_to_gray(self, rgb: np.ndarray) -> np.ndarray:
         """Rec. 601 integer luma of an (h, w, 3) u8 image on the GPU, as the

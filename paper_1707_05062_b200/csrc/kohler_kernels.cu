@@ -1819,6 +1819,16 @@ struct kohler_cuda_ctx {
     DevBuf stage;    // 16-byte aligned copy of unaligned device inputs for K1
     HostBuf hout;    // pinned staging for small results (one D2H per call)
     DevBuf rgb;      // staging for host RGB images (colour ingest)
+    // streaming host API (kohler_cuda_submit / kohler_cuda_collect): two
+    // slots of device image + packed results + pinned host results
+    DevBuf simg[2];
+    DevBuf sout[2];
+    HostBuf shout[2];
+    cudaEvent_t sup[2] = {};    // slot's upload finished (copy stream)
+    cudaEvent_t sdone[2] = {};  // slot's results are in shout (compute stream)
+    long long sticket = 0;      // next ticket
+    long long spend[2] = {-1, -1};  // ticket in flight per slot
+    int sn[2] = {}, sk[2] = {};     // its image count and k
     DevBuf gray;     // luma of device RGB inputs (16-byte pitched)
     DevBuf seg;      // segmentation scratch (histograms, thresholds)
     int last_launches = 0;
@@ -2633,6 +2643,11 @@ int kohler_cuda_create(int device, kohler_cuda_ctx** out)
         e = cudaEventCreateWithFlags(&ctx->chunk_ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess)
         e = cudaEventCreateWithFlags(&ctx->done_ev, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ctx->sup[i], cudaEventDisableTiming);
+        if (e == cudaSuccess)
+            e = cudaEventCreateWithFlags(&ctx->sdone[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
         delete ctx;
         return fail(KOHLER_CUDA_ERROR, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
@@ -2664,6 +2679,15 @@ void kohler_cuda_destroy(kohler_cuda_ctx* ctx)
         for (int i = 0; i < kMaxChunks; ++i)
             if (ctx->chunk_ev[i])
                 cudaEventDestroy(ctx->chunk_ev[i]);
+        for (int i = 0; i < 2; ++i) {
+            if (ctx->sup[i])
+                cudaEventDestroy(ctx->sup[i]);
+            if (ctx->sdone[i])
+                cudaEventDestroy(ctx->sdone[i]);
+            ctx->simg[i].release();
+            ctx->sout[i].release();
+            ctx->shout[i].release();
+        }
         if (ctx->done_ev)
             cudaEventDestroy(ctx->done_ev);
     }
@@ -2787,6 +2811,107 @@ int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, in
                            static_cast<cudaStream_t>(stream));
     return launch_wide(ctx, px, n, w, h, h, 0, pitch, image_stride, k, select ? 1 : 0, o,
                        static_cast<cudaStream_t>(stream));
+}
+
+int kohler_cuda_submit(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, size_t pitch,
+                       size_t image_stride, int k, long long* ticket)
+{
+    if (!ctx || !ticket || (!px && n > 0))
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    int rc = check_image(n, w, h, pitch);
+    if (rc)
+        return rc;
+    if (n < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "submit: at least one image");
+    if (k < 1)
+        return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (n > 1 && image_stride < pitch * (size_t)h)
+        return fail(KOHLER_INVALID_ARGUMENT, "image stride smaller than one image");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    const int slot = (int)(ctx->sticket & 1);
+    if (ctx->spend[slot] >= 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "submit: collect the ticket submitted two calls ago first");
+    const size_t dpitch = round_up((size_t)w, 16), dstride = dpitch * (size_t)h;
+    const size_t n256 = (size_t)n * 256;
+    const size_t tail_off = round_up(n256 * 25, 16);
+    const size_t bytes = tail_off + (size_t)n * 4 * 3 + (size_t)n * k * 4;
+    if ((rc = ctx->simg[slot].ensure(dstride * (size_t)n)) || (rc = ctx->sout[slot].ensure(bytes + 64)) ||
+        (rc = ctx->shout[slot].ensure(bytes)))
+        return rc;
+    uint8_t* dimg = static_cast<uint8_t*>(ctx->simg[slot].p);
+    cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
+    ctx->last_launches = 0;
+    // the upload overlaps the previous submission's kernels (other slot)
+    if (pitch == dpitch && (n == 1 || image_stride == dstride))
+        KC_CUDA(cudaMemcpyAsync(dimg, px, dstride * (size_t)n, cudaMemcpyHostToDevice, cs));
+    else if (n == 1 || image_stride == pitch * (size_t)h)
+        KC_CUDA(cudaMemcpy2DAsync(dimg, dpitch, px, pitch, (size_t)w, (size_t)h * n,
+                                  cudaMemcpyHostToDevice, cs));
+    else
+        for (int i = 0; i < n; ++i)
+            KC_CUDA(cudaMemcpy2DAsync(dimg + dstride * i, dpitch, px + image_stride * i, pitch,
+                                      (size_t)w, (size_t)h, cudaMemcpyHostToDevice, cs));
+    KC_CUDA(cudaEventRecord(ctx->sup[slot], cs));
+    KC_CUDA(cudaStreamWaitEvent(st, ctx->sup[slot], 0));
+    char* b = static_cast<char*>(ctx->sout[slot].p);
+    BatchOut d{};
+    d.sums = reinterpret_cast<uint64_t*>(b);
+    d.cards = reinterpret_cast<uint64_t*>(b + n256 * 8);
+    d.values = reinterpret_cast<double*>(b + n256 * 16);
+    d.defined = reinterpret_cast<uint8_t*>(b + n256 * 24);
+    d.t0s = reinterpret_cast<int*>(b + tail_off);
+    d.topk_counts = d.t0s + n;
+    d.status = d.topk_counts + n;
+    d.topks = d.status + n;
+    rc = use_tile(n, w, h) ? launch_tile(ctx, dimg, n, w, h, dpitch, dstride, k, 1, d, st)
+                           : launch_wide(ctx, dimg, n, w, h, h, 0, dpitch, dstride, k, 1, d, st);
+    if (rc)
+        return rc;
+    KC_CUDA(cudaMemcpyAsync(ctx->shout[slot].p, b, bytes, cudaMemcpyDeviceToHost, st));
+    KC_CUDA(cudaEventRecord(ctx->sdone[slot], st));
+    ctx->spend[slot] = ctx->sticket;
+    ctx->sn[slot] = n;
+    ctx->sk[slot] = k;
+    *ticket = ctx->sticket++;
+    return KOHLER_OK;
+}
+
+int kohler_cuda_collect(kohler_cuda_ctx* ctx, long long ticket, uint64_t* sums, uint64_t* cards,
+                        double* values, uint8_t* defined, int* t0s, int* topks, int* topk_counts,
+                        int* status)
+{
+    if (!ctx || ticket < 0)
+        return fail(KOHLER_INVALID_ARGUMENT, "NULL argument / bad ticket");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    const int slot = (int)(ticket & 1);
+    if (ctx->spend[slot] != ticket)
+        return fail(KOHLER_INVALID_ARGUMENT, "collect: no such ticket in flight");
+    KC_CUDA(cudaEventSynchronize(ctx->sdone[slot]));
+    const int n = ctx->sn[slot], k = ctx->sk[slot];
+    const size_t n256 = (size_t)n * 256;
+    const size_t tail_off = round_up(n256 * 25, 16);
+    const char* hb = static_cast<const char*>(ctx->shout[slot].p);
+    if (sums)
+        std::memcpy(sums, hb, n256 * 8);
+    if (cards)
+        std::memcpy(cards, hb + n256 * 8, n256 * 8);
+    if (values)
+        std::memcpy(values, hb + n256 * 16, n256 * 8);
+    if (defined)
+        std::memcpy(defined, hb + n256 * 24, n256);
+    const int* ht = reinterpret_cast<const int*>(hb + tail_off);
+    if (t0s)
+        std::memcpy(t0s, ht, (size_t)n * 4);
+    if (topk_counts)
+        std::memcpy(topk_counts, ht + n, (size_t)n * 4);
+    if (status)
+        std::memcpy(status, ht + 2 * n, (size_t)n * 4);
+    if (topks)
+        std::memcpy(topks, ht + 3 * n, (size_t)n * k * 4);
+    ctx->spend[slot] = -1;
+    return KOHLER_OK;
 }
 
 int kohler_cuda_rgb_to_gray_device(kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, int h,

@@ -190,3 +190,37 @@ def test_pipelined_back_to_back_calls(ref, depth):
     check_against_reference(want[0], exp)
     with pytest.raises(ValueError):
         cp.set_pipeline_depth(5)
+
+
+def test_streaming_submit_collect(ctx, ref):
+    """kohler_cuda_submit / kohler_cuda_collect: two tickets in flight, results
+    identical to the synchronous host API and to the reference; a third
+    submit before collecting fails; batches and ragged widths."""
+    x = synth.generate("C2", device="cpu")[0]
+    imgs = [x, x.flip(0), 255 - x, x[:, :5000], x[:777, :1231]]
+    pinned = [im.contiguous().pin_memory() for im in imgs]
+    want = [ctx.analyze_batch(im.numpy(), k=K) for im in imgs]
+    t_prev = ctx.submit(pinned[0], K)
+    got = []
+    for i in range(1, len(pinned)):
+        t = ctx.submit(pinned[i], K)
+        got.append(ctx.collect(t_prev))
+        t_prev = t
+    got.append(ctx.collect(t_prev))
+    for g, e in zip(got, want):
+        assert np.array_equal(g.sums, e.sums) and np.array_equal(g.cards, e.cards)
+        assert np.array_equal(g.values, e.values)
+        assert g.thresholds(0) == e.thresholds(0) and int(g.t0[0]) == int(e.t0[0])
+    ex = ref.analyze(x.numpy(), k=K, workers=8)
+    assert np.array_equal(got[0].sums[0], ex["sum"]) and got[0].thresholds(0) == ex["topk"]
+    a = ctx.submit(pinned[0], K)
+    b = ctx.submit(pinned[1], K)
+    with pytest.raises(ValueError):
+        ctx.submit(pinned[2], K)
+    ctx.collect(a)
+    ctx.collect(b)
+    batch = synth.generate("C5", device="cpu", n=64)
+    t = ctx.submit(batch.numpy(), K)
+    r = ctx.collect(t)
+    w5 = ctx.analyze_batch(batch.numpy(), k=K)
+    assert np.array_equal(r.sums, w5.sums) and np.array_equal(r.status, w5.status)
