@@ -397,6 +397,7 @@ def main():
             e2e = measure_e2e(ctx, img, args)
         else:
             e2e = e2e_bands
+        if world == 1:  # the CPU baseline: rank 0 at N=1 only
             med, runs, cores, kern = cpu_reference_time(img.numpy(), args.cpu_budget, 2000)
             cpu = {"value": w * h / med / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": f"full {CONFIG_NAME} image, median of {runs} runs (1 warm-up), "
