@@ -1,0 +1,49 @@
+"""bench.py's JSON line carries every key of the driver contract (a short
+run): the N=1 device line with roofline / cpu_baseline / e2e / clocks, and
+the reference arm's line."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(*args):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_device_line_keys():
+    d = run("--steps", "120", "--warmup", "3", "--e2e-steps", "5", "--cpu-budget", "1")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 120 and d["value"] > 0
+    assert d["config"]["workload"].startswith("C2 5184x3456")
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    c = d["cpu_baseline"]
+    assert c and c["kind"] == "reference" and c["value"] > 0 and c["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 5184 * 3456 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 2 * 120
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_reference_arm_line():
+    d = run("--impl", "reference", "--steps", "2", "--warmup", "1")
+    if "unavailable" in d:
+        pytest.skip(d["unavailable"])
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "reference"
+    assert d["config"]["workload"].startswith("C2 5184x3456")
