@@ -583,6 +583,37 @@ __device__ __forceinline__ void read_row(kohler_walk::Row& r, uint32_t seg, uint
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r.rn) : "r"(seg + offr) : "memory");
 }
 
+// Neighbour bytes by warp shuffles instead of byte loads: 16-byte-strided
+// LDS.U8 from 32 lanes is a 4-way bank conflict (5 wavefronts each, ~10 of a
+// step's ~65 MIO wavefronts); two SHFL + one single-lane pad load cost 3.
+// Per lane and segment: the left neighbour is the pixel itself (row start),
+// the pad byte (first lane of a run, not at a row start) or the previous
+// lane's last byte; the right one likewise (row end / last lane / next lane).
+struct NbrSel {
+    uint32_t pad_off;  // shared offset of this lane's pad byte from its segment (if any)
+    bool pad;          // lane reads a pad byte
+    bool l_own, l_pad;
+    bool r_own, r_pad;
+};
+
+__device__ __forceinline__ void read_row_shfl(kohler_walk::Row& r, uint32_t seg, const NbrSel& n)
+{
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                 : "r"(seg)
+                 : "memory");
+    uint32_t pb = 0;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+                 "@p ld.shared.u8 %0, [%2];\n\t}"
+                 : "+r"(pb)
+                 : "r"((uint32_t)n.pad), "r"(seg + n.pad_off)
+                 : "memory");
+    const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, r.w[3], 1);
+    const uint32_t dn = __shfl_down_sync(0xFFFFFFFFu, r.w[0], 1);
+    r.ln = n.l_own ? (r.w[0] & 0xFFu) : n.l_pad ? pb : (up >> 24);
+    r.rn = n.r_own ? (r.w[3] >> 24) : n.r_pad ? pb : (dn & 0xFFu);
+}
+
 // Per-group, warp-uniform flags.
 struct GroupFlags {
     bool edge;    // some lane is at a row start or row end (corr terms)
@@ -692,8 +723,13 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         const bool row_start = G.x0 == 0, row_end = G.e <= 15;
         // neighbour bytes: the adjacent lane's segment, lanes 0 / 31 their pad,
         // a row start / end the pixel itself
-        const uint32_t offl = G.x0 == 0 ? 0u : lane == 0 ? 512u + 15u : 0xFFFFFFFFu;
-        const uint32_t offr = G.e <= 15 ? 15u : lane == 31 ? 528u - 16u * 31u : 16u;
+        NbrSel nb;
+        nb.l_own = G.x0 == 0;
+        nb.l_pad = !nb.l_own && lane == 0;
+        nb.r_own = G.e <= 15;
+        nb.r_pad = !nb.r_own && lane == 31;
+        nb.pad = nb.l_pad || nb.r_pad;
+        nb.pad_off = lane == 0 ? 512u + 15u : 528u - 16u * 31u;
 
         // One ring position j: prefetch position j + 3 (of this segment or,
         // past its end, of the next), absorb row r0 - 1 + j into D and
@@ -711,7 +747,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             // read this position's row first: the prefetch issue below
             // covers the LDS latency before the unpack needs the data
             Row r;
-            read_row(r, sl_cur, offl, offr);
+            read_row_shfl(r, sl_cur, nb);
             const uint32_t pref = sl_prev;
             sl_prev = sl_cur;
             sl_cur = sl_cur + kSlotBytes == slot_end ? seg0 : sl_cur + kSlotBytes;
