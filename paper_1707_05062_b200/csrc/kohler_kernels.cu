@@ -568,21 +568,6 @@ __device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint3
     --f.left;
 }
 
-// Read ring slot position of this lane back: the segment and its neighbour
-// bytes (a row start's left / a row end's right neighbour is the pixel
-// itself: equal => neutral; lanes next to each other in a warp are
-// horizontal neighbours unless a row boundary lies between them).
-__device__ __forceinline__ void read_row(kohler_walk::Row& r, uint32_t seg, uint32_t offl,
-                                         uint32_t offr)
-{
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
-                 : "r"(seg)
-                 : "memory");
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r.ln) : "r"(seg + offl) : "memory");
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r.rn) : "r"(seg + offr) : "memory");
-}
-
 // Neighbour bytes by warp shuffles instead of byte loads: 16-byte-strided
 // LDS.U8 from 32 lanes is a 4-way bank conflict (5 wavefronts each, ~10 of a
 // step's ~65 MIO wavefronts); two SHFL + one single-lane pad load cost 3.
@@ -1044,8 +1029,13 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         LaneGeo N = G;
         const GroupFlags F = group_flags(G, ALIGNED);
         const bool row_start = G.x0 == 0, row_end = G.e <= 15;
-        const uint32_t offl = G.x0 == 0 ? 0u : lig == 0 ? padl + 15u : 0xFFFFFFFFu;
-        const uint32_t offr = G.e <= 15 ? 15u : lig == LG - 1 ? padr : 16u;
+        NbrSel nb;  // neighbour bytes: shuffles inside the group, pads at its ends
+        nb.l_own = G.x0 == 0;
+        nb.l_pad = !nb.l_own && lig == 0;
+        nb.r_own = G.e <= 15;
+        nb.r_pad = !nb.r_own && lig == LG - 1;
+        nb.pad = nb.l_pad || nb.r_pad;
+        nb.pad_off = lig == 0 ? padl + 15u : padr;
         auto step = [&](Car& D, Car& C, int j, auto kind, auto wc, auto cross) {
             constexpr int KIND = decltype(kind)::value;
             constexpr int WC = decltype(wc)::value;
@@ -1055,7 +1045,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             __syncwarp();
             Row r;  // read first: the prefetch issue covers the LDS latency
-            read_row(r, seg0 + (q & 3u) * Lay::kSlot, offl, offr);
+            read_row_shfl(r, seg0 + (q & 3u) * Lay::kSlot, nb);
             const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
             if (!CROSS || j + 3 < P)
                 fetch_row(G, j + 3, pitch, pref);
