@@ -154,8 +154,9 @@ def test_host_api_chunked_batch_vs_reference(ctx, ref):
 def test_pipelined_back_to_back_calls(ref, depth):
     """Pipeline depth d (kohler_cuda_set_pipeline_depth): d consecutive
     accumulation launches run side by side (sharing one accumulator buffer:
-    each flush waits for the previous finish_kernel).  Back-to-back calls on different images must give exactly the
-    depth-1 results (and the reference's on the C2 image)."""
+    each flush waits for the previous finish_kernel).  Back-to-back calls on
+    different images must give exactly the depth-1 results (and the
+    reference's on the C2 image)."""
     from paper_1707_05062_b200 import Context
     x = synth.generate("C2", device="cuda")[0]
     imgs = [x, x.flip(0).contiguous(), x.flip(1).contiguous(), (255 - x).contiguous(),
@@ -224,3 +225,26 @@ def test_streaming_submit_collect(ctx, ref):
     r = ctx.collect(t)
     w5 = ctx.analyze_batch(batch.numpy(), k=K)
     assert np.array_equal(r.sums, w5.sums) and np.array_equal(r.status, w5.status)
+
+
+def test_image_larger_than_4_gib(ctx):
+    """A 65600 x 65536 image (4.3 GB, > 2^32 bytes): 64-bit addressing in the
+    walk, the border pass and the band split; checked through the identities
+    (card total = total variation, sum total = Σ⌊Δ²/4⌋) and the invariants."""
+    h, w = 65600, 65536
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0x4B)
+    x = torch.randint(0, 256, (h, w), dtype=torch.uint8, device="cuda", generator=g)
+    x[: h // 3] //= 5
+    r = run_batch(ctx, x[None])
+    tv = qs = 0
+    for y0 in range(0, h, 2048):
+        a = x[y0:min(y0 + 2049, h)].to(torch.int32)
+        dx = (a[:min(2048, h - y0), 1:] - a[:min(2048, h - y0), :-1]).abs()
+        dy = (a[1:] - a[:-1]).abs()
+        for d in (dx, dy):
+            tv += int(d.sum(dtype=torch.int64))
+            qs += int((d * d // 4).sum(dtype=torch.int64))
+        del a, dx, dy
+    check_invariants(r, np.array([tv]), np.array([qs]))
+    assert int(r["status"][0]) == 0
