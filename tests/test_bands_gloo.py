@@ -158,3 +158,69 @@ def test_gloo_pipelined_steps(orc, world):
     want = [(e["t0"], e["topk"]) for e in (orc.analyze(im, 6) for im in imgs)]
     for _, got in res:
         assert got == want
+
+
+class _OracleBatchCtx:
+    """CPU stand-in of Context.analyze_batch_device: the oracle pipeline per
+    image, written into the output tensors."""
+
+    def __init__(self, orc):
+        self.orc = orc
+
+    def analyze_batch_device(self, x, w, h, pitch, stride, n, k, out, stream=None):
+        for i in range(n):
+            e = self.orc.analyze(x[i].numpy(), k)
+            out["sums"][i] = torch.from_numpy(e["sum"].view(np.int64))
+            out["cards"][i] = torch.from_numpy(e["card"].view(np.int64))
+            out["t0"][i] = e["t0"]
+            out["topk_count"][i] = len(e["topk"])
+            out["topk"][i, : len(e["topk"])] = torch.tensor(e["topk"], dtype=torch.int32)
+            out["status"][i] = e["status"]
+
+
+def _worker_shard(rank, world, port, imgs, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1707_05062_b200.shard import BatchSharder
+    n, h, w = imgs.shape
+    sh = BatchSharder(_OracleBatchCtx(oracle.Oracle()), n, w, h, world, rank, k,
+                      device=torch.device("cpu"))
+    full = sh.run(torch.from_numpy(imgs[sh.i0:sh.i1]), gather=True)
+    q.put((rank, {key: v.numpy().copy() for key, v in full.items()}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_batch_shards_and_gather(orc, world):
+    """C3 / C5-style sharding: contiguous image shards (sizes differing by
+    one), no collective but the optional all-gather, results in batch order
+    on every rank, identical to the single-process pipeline."""
+    from paper_1707_05062_b200.shard import shard_bounds
+    for n in (1, 2, 7, 64):
+        sizes = [shard_bounds(n, world, r)[1] - shard_bounds(n, world, r)[0] for r in range(world)]
+        assert sum(sizes) == n and max(sizes) - min(sizes) <= 1
+    rng = np.random.default_rng(7 + world)
+    n = 7
+    imgs = rng.integers(0, 256, (n, 19, 23), dtype=np.uint8)
+    imgs[2] = 40  # a no-boundary image
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_shard, args=(r, world, port, imgs, 6, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, full in res:
+        for i in range(n):
+            e = orc.analyze(imgs[i], 6)
+            assert np.array_equal(full["sums"][i].view(np.uint64), e["sum"])
+            assert int(full["t0"][i]) == e["t0"] and int(full["status"][i]) == e["status"]
+            cnt = int(full["topk_count"][i])
+            assert list(full["topk"][i, :cnt]) == e["topk"]
