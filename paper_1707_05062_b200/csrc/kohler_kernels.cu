@@ -1026,6 +1026,12 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
     bool waited = false;
     Car X, Y;
     uint32_t pos = 0;
+#ifdef KOHLER_PHASES  // tools/tile_probe.cu: per-CTA cycles of the round phases
+    long long tw_t = clock64(), tw_acc[5] = {0, 0, 0, 0, 0};
+#define TWCYC(i) do { const long long t_ = clock64(); tw_acc[i] += t_ - tw_t; tw_t = t_; } while (0)
+#else
+#define TWCYC(i) do { } while (0)
+#endif
     for (; i0 < p.n; i0 += stride) {
         const bool has_next = i0 + stride < p.n;
         LaneGeo N = G;
@@ -1149,6 +1155,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             }
         }
         __syncthreads();
+        TWCYC(0);  // walk (incl. the wait for the slowest warp)
         if (!waited) {
             pdl_wait();  // the previous launch may still read our outputs
             waited = true;
@@ -1180,6 +1187,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 vb[q] = b;
             }
             __syncthreads();
+            TWCYC(1);
             // 2. per-image totals into a padded scratch carved out of the (now
             //    zero) counter block: hs[s] at s + s/16, the other arrays at
             //    x + x/8 (conflict-free lane-blocked reads of warp_curve256)
@@ -1199,6 +1207,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 }
             }
             __syncthreads();
+            TWCYC(2);
             if (warp < NG && i0 + warp < p.n) {
                 // 3. K3 for image i0 + warp
                 const uint32_t* base = scr + warp * kTwImgWords;
@@ -1239,6 +1248,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 }
             }
             __syncthreads();
+            TWCYC(3);
             // 4. clear the scratch and the border terms for the next round
             uint4* z = reinterpret_cast<uint4*>(hist);
             for (int i = tid; i < NG * kTwImgWords / 4; i += kTwThreads)
@@ -1247,9 +1257,16 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
         __syncthreads();
+        TWCYC(4);
         pos += (uint32_t)P;
         G = N;
     }
+#ifdef KOHLER_PHASES
+    if (threadIdx.x == 0 && blockIdx.x < 2048)
+        for (int i = 0; i < 5; ++i)
+            g_phase[blockIdx.x][i] = (unsigned long long)tw_acc[i];
+#endif
+#undef TWCYC
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (!waited)
         pdl_wait();

@@ -1,6 +1,6 @@
 // Debug probe of the K5 tile kernel: per-CTA clock64 totals of the
 // accumulation phase, the reduce phase, and the rest, for n images of w x h.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DKOHLER_PHASES -Iinclude -o tools/tile_probe tools/tile_probe.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DKOHLER_PHASES -DKOHLER_WALK_THREADS=512 -Iinclude -o tools/tile_probe tools/tile_probe.cu
 #include "../paper_1707_05062_b200/csrc/kohler_kernels.cu"
 #include <vector>
 int main(int argc, char** argv)
@@ -22,10 +22,11 @@ int main(int argc, char** argv)
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); printf("batch %.3f ms (%.1f Gpx/s)\n", ms, (double)n * w * h / ms / 1e6);
     }
-    static unsigned long long ph[2048][8];
+    static unsigned long long ph[2048][12];
     cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
-    double acc = 0, red = 0, rest = 0; int G = 148;
-    for (int c = 0; c < G; ++c) { acc += ph[c][0]; red += ph[c][1]; rest += ph[c][2]; }
-    printf("per CTA cycles: accumulate %.0f, reduce %.0f, other %.0f\n", acc / G, red / G, rest / G);
+    double t[5] = {0}; int G = 147;
+    for (int c = 0; c < G; ++c) for (int i = 0; i < 5; ++i) t[i] += ph[c][i];
+    printf("K5 per-CTA cycles: walk %.0f, read+clear %.0f, scratch %.0f, K3 %.0f, clear %.0f\n",
+           t[0] / G, t[1] / G, t[2] / G, t[3] / G, t[4] / G);
     return 0;
 }
