@@ -1,19 +1,24 @@
 // kohler_kernels.cu — sm_100a kernels of the Köhler contrast-curve path and
-// the C ABI (include/kohler_cuda.h) that launches them.
+// the C ABI (include/kohler_cuda.h) that launches them.  DESIGN.md §3 has
+// the full description; in short:
 //
-//   K1  wide_kernel    : persistent, one 1024-thread CTA per SM; each CTA owns
-//                        a contiguous range of 16-pixel segments (flattened
-//                        row-major over the batch), accumulates them into a
-//                        lane-striped 128 KiB shared histogram (kohler_device.cuh),
-//                        and at every image boundary flushes 512 exact linear
-//                        combinations to global u64 accumulators (REDG.ADD.64).
-//   K3  (tail of K1)   : the last CTA to flush an image (atomic ticket) sums
-//                        the accumulator copies, rebuilds count/sum with int64
-//                        prefix scans and resets the workspace for the next launch.
-//   K4  (tail of K1) / select_kernel : mean curve (IEEE f64 divide), optimal
-//                        threshold, top-k local maxima, on device.
-//
-// The whole per-image pipeline is therefore ONE launch.
+//   K1  walk_kernel    : persistent, one 512-thread CTA per SM (or 1/d of the
+//                        SMs in pipelined mode); every lane walks down a
+//                        16-pixel column segment, rows streamed through a
+//                        cp.async ring, three shared atomics per pixel into a
+//                        lane-striped 128 KiB counter block (kohler_walk.cuh);
+//                        the CTA flush turns the counters into 512 exact
+//                        integer combinations, REDG.ADD.64 into the image's
+//                        accumulators.
+//   K3/K4 finish_kernel: PDL-chained after K1, one CTA per image: sums and
+//                        resets the accumulators, int64 prefix scans (count,
+//                        sum), IEEE f64 mean curve, optimal threshold, top-k.
+//   K5  twalk_kernel   : batches of small images (lane groups own images;
+//                        curves rebuilt in the CTA), + select256_kernel (K4).
+//   select_kernel / select256_kernel : selection on given curves.
+//   direct_kernel      : definition-level curve (direct.cpp restated).
+//   hist_kernel / map_kernel : segmentation (classify / quantize).
+//   luma_kernel        : Rec. 601 colour ingest.
 #include <cuda_runtime.h>
 
 #include <algorithm>
