@@ -25,6 +25,7 @@
 #include "kohler/contrast.hpp"
 #include "kohler/curve.hpp"
 #include "kohler/image.hpp"
+#include "kohler/stream.hpp"
 #include "kohler/threshold.hpp"
 #include "kohler_cuda.h"
 
@@ -185,5 +186,65 @@ GrayImage quantize(const GrayImage& img, const ThresholdSet& ts)
                                    static_cast<int>(ts.thresholds.size()), out.pixels().data()));
     return out;
 }
+
+namespace b200 {
+
+// the frame a ticket borrows (kept alive by the caller until collect)
+struct FrameStream::Slot {
+    long long ticket;
+};
+
+FrameStream::FrameStream(int k) : k_(k)
+{
+    if (k < 1)
+        throw std::invalid_argument("top_k_local_maxima: k must be at least 1");
+}
+
+FrameStream::~FrameStream()
+{
+    for (Slot* s : slots_) {  // drain what was never collected
+        kohler_cuda_collect(context(), s->ticket, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, nullptr);
+        delete s;
+    }
+}
+
+long long FrameStream::submit(const GrayImage& frame)
+{
+    long long t = -1;
+    raise_for(kohler_cuda_submit(context(), frame.row(0), 1, frame.width(), frame.height(),
+                                 static_cast<std::size_t>(frame.width()), 0, k_, &t));
+    slots_.push_back(new Slot{t});
+    return t;
+}
+
+FrameResult FrameStream::collect(long long ticket)
+{
+    FrameResult r;
+    std::vector<double> vals(256);
+    std::vector<std::uint8_t> def(256);
+    std::vector<int> topk(static_cast<std::size_t>(k_));
+    int t0 = -1, cnt = 0, status = 0;
+    raise_for(kohler_cuda_collect(context(), ticket, r.curve.contrast_sum.data(),
+                                  r.curve.cardinality.data(), vals.data(), def.data(), &t0,
+                                  topk.data(), &cnt, &status));
+    for (std::size_t i = 0; i < slots_.size(); ++i)
+        if (slots_[i]->ticket == ticket) {
+            delete slots_[i];
+            slots_.erase(slots_.begin() + static_cast<std::ptrdiff_t>(i));
+            break;
+        }
+    r.mean.values = vals;
+    r.mean.defined.resize(256);
+    for (int t = 0; t < 256; ++t)
+        r.mean.defined[t] = def[t] != 0;
+    r.has_boundary = status == KOHLER_OK;
+    r.optimal_threshold = r.has_boundary ? t0 : -1;
+    if (r.has_boundary)
+        r.top_k.thresholds.assign(topk.begin(), topk.begin() + cnt);
+    return r;
+}
+
+} // namespace b200
 
 } // namespace kohler

@@ -14,6 +14,7 @@
 #include "kohler/contrast.hpp"
 #include "kohler/curve.hpp"
 #include "kohler/image.hpp"
+#include "kohler/stream.hpp"
 #include "kohler/threshold.hpp"
 
 extern "C" void oracle_fast_curve(const uint8_t* px, int w, int h, uint64_t* sum, uint64_t* card);
@@ -140,6 +141,47 @@ int main()
         CHECK(g.contrast_sum == s && g.cardinality == c);
         CHECK(fast_contrast_curve(img, 7) == g);
         CHECK(direct_contrast_curve(img) == g);
+    }
+    // FrameStream (two frames in flight) == the synchronous functions
+    {
+        std::vector<GrayImage> frames;
+        for (int f = 0; f < 6; ++f) {
+            const int w = 640 + 16 * f, h = 360;
+            std::vector<std::uint8_t> px((std::size_t)w * h);
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x)
+                    px[(std::size_t)y * w + x] =
+                        (std::uint8_t)(((x / (40 + f)) + (y / 30)) % 2 ? 200 : 40) + (std::uint8_t)(rng() % 7);
+            frames.emplace_back(w, h, px);
+        }
+        frames.emplace_back(64, 48, 9);  // no boundary
+        b200::FrameStream fs(6);
+        std::vector<b200::FrameResult> got;
+        long long prev = fs.submit(frames[0]);
+        for (std::size_t f = 1; f < frames.size(); ++f) {
+            const long long t = fs.submit(frames[f]);
+            got.push_back(fs.collect(prev));
+            prev = t;
+        }
+        got.push_back(fs.collect(prev));
+        for (std::size_t f = 0; f < frames.size(); ++f) {
+            const ContrastCurve c = fast_contrast_curve(frames[f]);
+            CHECK(got[f].curve == c);
+            const MeanContrastCurve mc = mean_contrast(c);
+            CHECK(got[f].mean.values == mc.values && got[f].mean.defined == mc.defined);
+            if (got[f].has_boundary) {
+                CHECK(got[f].optimal_threshold == optimal_threshold(mc));
+                CHECK(got[f].top_k == top_k_local_maxima(mc, 6));
+            } else {
+                CHECK(throws<NoBoundaryError>([&] { (void)optimal_threshold(mc); }));
+            }
+        }
+        CHECK(!got.back().has_boundary);
+        const long long a = fs.submit(frames[0]);
+        const long long b = fs.submit(frames[1]);
+        CHECK(throws<std::invalid_argument>([&] { (void)fs.submit(frames[2]); }));
+        (void)fs.collect(a);
+        (void)b;  // left in flight: the destructor drains it
     }
     if (g_fail) {
         std::fprintf(stderr, "%d of %d checks failed\n", g_fail, g_checks);
