@@ -17,6 +17,9 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--depth", type=int, default=1, help="kohler_cuda_set_pipeline_depth")
+ap.add_argument("--graph", type=int, default=0,
+                help="replay the timed loop from CUDA graphs of this many calls (launch-bound "
+                     "configs: removes the per-call Python/ctypes issue cost)")
 ap.add_argument("--rgb", action="store_true",
                 help="colour ingest: time the pipeline on an RGB version of the config "
                      "(channels: the grey map shifted by 3 px, itself, its negative)")
@@ -64,15 +67,30 @@ torch.cuda.synchronize()
 if a.time:
     steps = max(3, int(2e9 // max(x[0].numel(), 1)))
     steps = min(steps, 2000)
+    graph = None
+    if a.graph > 0:
+        a.graph = max(a.graph, copies)  # every input copy once per replay (L2 rotation)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(a.graph):
+                call(i)
+        graph.replay()
+        torch.cuda.synchronize()
+        steps = max(1, steps // a.graph) * a.graph
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(steps):
-        call(i)
+    if graph is not None:
+        for _ in range(steps // a.graph):
+            graph.replay()
+    else:
+        for i in range(steps):
+            call(i)
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / steps
     px = n * h * w
-    print(json.dumps({"config": a.config, "rgb": a.rgb, "depth": a.depth, "segment": a.segment, "n": n, "w": w, "h": h,
+    print(json.dumps({"config": a.config, "rgb": a.rgb, "depth": a.depth, "graph": a.graph,
+                      "segment": a.segment, "n": n, "w": w, "h": h,
                       "ms_per_step": ms,
                       "gpix_per_s": px / ms / 1e6, "hbm_frac": px / ms / 1e6 / 6452.8,
                       "images_per_s": n / ms * 1e3, "copies": copies, "steps": steps}))
