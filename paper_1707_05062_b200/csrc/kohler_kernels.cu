@@ -953,7 +953,8 @@ struct TwLayout {
     static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
     static constexpr uint32_t kRingBytes = kTwWarps * kRingSlots * kSlot + 128;
     static constexpr uint32_t kCorr = kRingBytes;  // int[NG][256]
-    static constexpr uint32_t kEnd = kCorr + NG * 1024;
+    static constexpr uint32_t kTot = kCorr + NG * 1024;  // i64 [3][16 warps][NG] scan carries
+    static constexpr uint32_t kEnd = kTot + 3 * 16 * NG * 8;
     static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
 };
 
@@ -1165,6 +1166,135 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             pdl_wait();  // the previous launch may still read our outputs
             waited = true;
         }
+        if constexpr (LG == 4) {
+            // Cooperative flush for 8 images per round (C5): warp w owns the
+            // keys [16 w, 16 w + 16) of all 8 images; lane L takes image
+            // L & 7, keys t0 .. t0 + 3 (t0 = 16 w + 4 (L >> 3)).  A group's 4
+            // lane words of a counter row are one 16-byte piece, and the 8
+            // lanes of a quarter warp (one LDS.128 wavefront) hit 8 bank quads, so
+            // the counters are read once, conflict free, straight into the
+            // per-image combinations; the scans run across the 4 lanes of an
+            // image and then across warps (two small carry exchanges).  No
+            // transposed scratch copy, no second clearing pass.
+            // (the 8 lanes of each quarter warp -- one LDS.128 wavefront --
+            // take 8 different images, i.e. 8 different bank quads)
+            const int gi = lane & 7, q4 = lane >> 3;
+            const int t0 = 16 * warp + 4 * q4;
+            auto grp = [&](int row, int half) -> uint4 {
+                return *reinterpret_cast<const uint4*>(hist + row * 256 + half * 128 + gi * 16);
+            };
+            auto wsum = [](const uint4& v, long long& h, long long& b) {
+                h += (long long)((v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu));
+                b += (long long)((v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16));
+            };
+            long long hv[5] = {0, 0, 0, 0, 0};  // hist(t0 - 1 + i)
+            long long cd[4], h2[4];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const int t = t0 - 1 + i;
+                long long hh = 0, bb = 0;
+                if (t >= 0) {
+                    wsum(grp(t, 1), hh, bb);        // W copy 0
+                    wsum(grp(256 + t, 1), hh, bb);  // W copy 1
+                }
+                hv[i] = hh;
+                if (i > 0)
+                    cd[i - 1] = bb - 4ll * hh;
+            }
+            long long hs[9];  // Hs rows 2 t0 - 3 .. 2 t0 + 5
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const int r = 2 * t0 - 3 + i;
+                long long v = 0;
+                if (r >= 0) {
+                    const uint4 c = grp(r, 0);
+                    v = (long long)c.x + c.y + c.z + c.w;
+                }
+                hs[i] = v;
+            }
+            const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + gi * 1024);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int u = t0 + i;  // h2(u) = 4 hist(u-1) - corr(u-1) - hs(2u-3) - 2 hs(2u-2) - hs(2u-1)
+                h2[i] = u == 0 ? 0
+                               : 4ll * hv[i] - (long long)cr[u - 1] - hs[2 * i] - 2ll * hs[2 * i + 1] -
+                                     hs[2 * i + 2];
+            }
+            // hs[0] (row 2 t0 - 3) is counted for u = t0 only when u >= 2: a
+            // negative row is 0 already, so the formula matches warp_curve256's
+            uint32_t hist_keep[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                hist_keep[i] = (uint32_t)hv[i + 1];
+            __syncthreads();  // every counter read: clear the block for the next round
+            {
+                uint4* z = reinterpret_cast<uint4*>(hist);
+                for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
+                    z[i] = make_uint4(0, 0, 0, 0);
+            }
+            // scans: lane-local, then across the image's 4 lanes (a quad)
+            long long* tot = reinterpret_cast<long long*>(sm + Lay::kTot);  // [3][16][NG]
+            auto quad_scan = [&](long long (&v)[4]) -> long long {
+#pragma unroll
+                for (int i = 1; i < 4; ++i)
+                    v[i] += v[i - 1];
+                long long x = v[3];  // the image's 4 lanes are gi, gi + 8, gi + 16, gi + 24
+#pragma unroll
+                for (int off = 1; off < 4; off <<= 1) {
+                    const long long y = __shfl_up_sync(0xFFFFFFFFu, x, 8 * off);
+                    if (q4 >= off)
+                        x += y;
+                }
+                const long long ex = x - v[3];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    v[i] += ex;
+                return __shfl_sync(0xFFFFFFFFu, x, 24 + gi);  // the image's (= warp's) total
+            };
+            const long long tc = quad_scan(cd);
+            const long long tg = quad_scan(h2);  // h2 -> g (sum first difference)
+            if (q4 == 0) {
+                tot[(0 * 16 + warp) * NG + gi] = tc;
+                tot[(1 * 16 + warp) * NG + gi] = tg;
+            }
+            __syncthreads();
+            long long cc = 0, cg = 0;
+            for (int w2 = 0; w2 < warp; ++w2) {
+                cc += tot[(0 * 16 + w2) * NG + gi];
+                cg += tot[(1 * 16 + w2) * NG + gi];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cd[i] += cc;  // card
+                h2[i] += cg;  // g
+            }
+            const long long ts = quad_scan(h2);  // g -> sum, without the carry of earlier warps' g
+            if (q4 == 0)
+                tot[(2 * 16 + warp) * NG + gi] = ts;
+            __syncthreads();
+            long long cs = 0;
+            for (int w2 = 0; w2 < warp; ++w2)
+                cs += tot[(2 * 16 + w2) * NG + gi];
+            const long long im = i0 + gi;
+            if (im < p.n) {
+                uint64_t* os = p.sums + (size_t)im * 256 + t0;
+                uint64_t* oc = p.cards + (size_t)im * 256 + t0;
+                *reinterpret_cast<ulonglong2*>(oc) = make_ulonglong2((uint64_t)cd[0], (uint64_t)cd[1]);
+                *reinterpret_cast<ulonglong2*>(oc + 2) = make_ulonglong2((uint64_t)cd[2], (uint64_t)cd[3]);
+                *reinterpret_cast<ulonglong2*>(os) =
+                    make_ulonglong2((uint64_t)(h2[0] + cs), (uint64_t)(h2[1] + cs));
+                *reinterpret_cast<ulonglong2*>(os + 2) =
+                    make_ulonglong2((uint64_t)(h2[2] + cs), (uint64_t)(h2[3] + cs));
+                if (p.hist_out) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        p.hist_out[(size_t)im * 256 + t0 + i] = hist_keep[i];
+                }
+            }
+            TWCYC(1);
+            for (int i = tid; i < NG * 256; i += kTwThreads)
+                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
+        } else
         {
             // 1. every thread: 2*NG (half-row, group) cells, contiguous 16-byte
             //    pieces across a warp (conflict free): read, sum the group's LG
