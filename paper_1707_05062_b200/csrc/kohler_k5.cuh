@@ -1,0 +1,504 @@
+// kohler_k5.cuh — K5 twalk_kernel: batches of small images.
+// Part of the single translation unit kohler_kernels.cu (included there,
+// in this order, after the shared constants and parameter blocks).
+#pragma once
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K5 twalk_kernel: batches of small images with the three-event column walk.
+// The 32 lanes of every warp are split into NG = 32/LG lane groups; group g
+// of all 16 warps walks image i0 + g of the round, so the image's counters
+// are exactly its LG lane stripes of the shared block (conflict free across
+// images) and one round accumulates NG whole images.  Walker (warp w, lane
+// l in group g) takes task w*LG + l of its image: segment column task % S,
+// rows [R*(task/S), +R).  Each group's first / last lane also copies the 16
+// bytes left / right of the group's run into the group's pads.  After the
+// walk, warp g rebuilds image i0+g's curve straight from its stripes (K3) and
+// zeroes them; the per-image selection runs in select_kernel (K4).
+// ---------------------------------------------------------------------------
+struct TwParams {
+    const uint8_t* px;
+    size_t pitch;
+    size_t image_stride;
+    int n, w, h;
+    int S;  // segments per row
+    int R;  // rows per walk
+    int C;  // walk chunks per image (S * C <= 16 * LG)
+    uint64_t* sums;
+    uint64_t* cards;
+    uint32_t* hist_out;  // [n][256] pixel histogram, or null
+};
+
+// K5 per-image totals scratch (u32, padded): hs[512] at pad16, then
+// h0, b0, h1, b1 [256] at pad8 (kTwArr words each)
+constexpr int kTwArr = 288;                               // pad8(255) = 286
+constexpr int kTwH = 560;                                 // pad16(511) = 542
+__device__ __forceinline__ int pad8(int x) { return x + (x >> 3); }    // 9*lane + j: conflict free
+__device__ __forceinline__ int pad16(int x) { return x + (x >> 4); }   // 17*lane + c
+constexpr int kTwImgWords = (kTwH + 4 * kTwArr + 3) / 4 * 4;
+
+template <int LG>
+struct TwLayout {
+    static constexpr int NG = 32 / LG;
+    // 32 lane segments (512 B, 128-byte aligned), then 2 pads per group
+    static constexpr uint32_t kSlot = (512 + 32 * NG + 127) / 128 * 128;
+    static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
+    static constexpr uint32_t kRingBytes = kTwWarps * kRingSlots * kSlot + 128;
+    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][256]
+    static constexpr uint32_t kTot = kCorr + NG * 1024;  // i64 [3][16 warps][NG] scan carries
+    static constexpr uint32_t kEnd = kTot + 3 * 16 * NG * 8;
+    static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
+};
+
+__device__ __forceinline__ LaneGeo tw_geo(const TwParams& p, long long img, int task)
+{
+    LaneGeo L;
+    const bool act = img < p.n && task < p.S * p.C;
+    const int s = act ? task % p.S : 0;
+    const int c = act ? task / p.S : 0;
+    L.x0 = s << 4;
+    L.e = p.w - 1 - L.x0;
+    if (act) {
+        L.y0 = c * p.R;
+        L.nrows = min(p.R, p.h - L.y0);
+        L.jlo = L.y0 == 0 ? 1 : 0;
+        L.jcl = p.h - L.y0;
+    } else {
+        L.y0 = 1;
+        L.nrows = 0;
+        L.jlo = 0;
+        L.jcl = 0;
+    }
+    L.p = p.px + (size_t)(act ? img : 0) * p.image_stride + (long long)(L.y0 - 1) * (long long)p.pitch +
+          L.x0;
+    return L;
+}
+
+template <bool ALIGNED, int LG>
+__global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
+{
+    using namespace kohler_walk;
+    using Lay = TwLayout<LG>;
+    constexpr int NG = Lay::NG;
+    extern __shared__ __align__(16) unsigned char sm[];
+    const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
+    if (smbase + Lay::kEnd > kHistAbs)
+        __trap();
+    unsigned char* hist = sm + (kHistAbs - smbase);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane / LG, lig = lane % LG;
+    const uint32_t lane4 = (uint32_t)lane * 4u;
+    const uint32_t kneg = kHistAbs - lane4;
+    const uint32_t dummy = kHistAbs + kDummy + lane4;
+    const uint32_t corr_g = smbase + Lay::kCorr + (uint32_t)g * 1024u;
+    const uint32_t corr_base = corr_g - (lane4 >> 6);
+    const uint32_t pitch = (uint32_t)p.pitch;
+    const int task = warp * LG + lig;
+    const int P = p.R + 2;
+    const uint32_t ring = (smbase + Lay::kRing + 127u) & ~127u;
+    const uint32_t seg0 = ring + (uint32_t)warp * (kRingSlots * Lay::kSlot) + (uint32_t)lane * 16u;
+    const uint32_t padl = 512u + 32u * g - 16u * lane;  // group pads, relative to the segment
+    const uint32_t padr = padl + 16u;
+    auto geo = [&](long long i0) {
+        LaneGeo L = tw_geo(p, i0 + g, task);
+        L.pd = lig == 0 ? -16 : 16;
+        L.pds = (int)(lig == 0 ? padl : padr);
+        L.pad = ((lig == 0) & (L.x0 > 0)) | ((lig == LG - 1) & (L.e > 15)) ? 1u : 0u;
+        return L;
+    };
+    const long long stride = (long long)gridDim.x * NG;
+    long long i0 = (long long)blockIdx.x * NG;
+    LaneGeo G = geo(i0);
+    fetch_row(G, 0, pitch, seg0);
+    fetch_row(G, 1, pitch, seg0 + Lay::kSlot);
+    fetch_row(G, 2, pitch, seg0 + 2 * Lay::kSlot);
+    {
+        uint4* z = reinterpret_cast<uint4*>(hist);
+        for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
+            z[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < NG * 256; i += kTwThreads)
+            reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
+    }
+    __syncthreads();
+    bool waited = false;
+    Car X, Y;
+    uint32_t pos = 0;
+#ifdef KOHLER_PHASES  // tools/tile_probe.cu: per-CTA cycles of the round phases
+    long long tw_t = clock64(), tw_acc[5] = {0, 0, 0, 0, 0};
+#define TWCYC(i) do { const long long t_ = clock64(); tw_acc[i] += t_ - tw_t; tw_t = t_; } while (0)
+#else
+#define TWCYC(i) do { } while (0)
+#endif
+    for (; i0 < p.n; i0 += stride) {
+        const bool has_next = i0 + stride < p.n;
+        LaneGeo N = G;
+        const GroupFlags F = group_flags(G, ALIGNED);
+        const bool row_start = G.x0 == 0, row_end = G.e <= 15;
+        NbrSel nb;  // neighbour bytes: shuffles inside the group, pads at its ends
+        nb.l_own = G.x0 == 0;
+        nb.l_pad = !nb.l_own && lig == 0;
+        nb.r_own = G.e <= 15;
+        nb.r_pad = !nb.r_own && lig == LG - 1;
+        nb.pad = nb.l_pad || nb.r_pad;
+        nb.pad_off = lig == 0 ? padl + 15u : padr;
+        auto step = [&](Car& D, Car& C, int j, auto kind, auto wc, auto cross) {
+            constexpr int KIND = decltype(kind)::value;
+            constexpr int WC = decltype(wc)::value;
+            constexpr bool CROSS = decltype(cross)::value;
+            constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
+            const uint32_t q = pos + (uint32_t)j;
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncwarp();
+            Row r;  // read first: the prefetch issue covers the LDS latency
+            read_row_shfl(r, seg0 + (q & 3u) * Lay::kSlot, nb);
+            const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
+            if (!CROSS || j + 3 < P)
+                fetch_row(G, j + 3, pitch, pref);
+            else if (has_next)
+                fetch_row(N, j + 3 - P, pitch, pref);
+            else
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            absorb<ALIGNED>(D, r, lane4, G.e);
+            if (KIND == 1) {
+                const bool has_up = G.y0 > 0;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    D.ue[jj] = has_up ? qstep(qfrom(C.e[jj]), D.e[jj]) : kNeutral;
+                    D.uo[jj] = has_up ? qstep(qfrom(C.o[jj]), D.o[jj]) : kNeutral;
+                }
+            }
+            if (KIND < 2)
+                return;
+            const bool live = j - 2 < G.nrows;
+            uint32_t qre[4], qro[4], qde[4], qdo[4], Be[4], Bo[4];
+            pair_q(C, D.e, D.o, qre, qro, qde, qdo);
+            b_terms(C, qre, qro, qde, qdo, Be, Bo);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                D.ue[jj] = qde[jj];
+                D.uo[jj] = qdo[jj];
+            }
+            const uint32_t Arn = __byte_perm(C.rn, lane4, 0x5504);
+            if (ALIGNED || !F.ragged) {
+                if (live) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_add_imm<kHistAbs + kOffW>(C.A[i], b_of(Be, Bo, i));
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        red_inc(C.A[i] + D.A[i] + kneg);
+                }
+            } else if (live) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const bool real = i <= G.e;
+                    red_add_imm<kHistAbs + kOffW>(C.A[i], real ? b_of(Be, Bo, i) : 0u);
+                    red_inc(real ? C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg : dummy);
+                    red_inc(real ? C.A[i] + D.A[i] + kneg : dummy);
+                }
+            }
+            if (F.edge && live) {
+                if (row_start)
+                    red_add(corr_base + (C.A[0] >> 6), 1u);
+                if (row_end)
+                    red_add(corr_base + (Arn >> 6), 0xFFFFFFFFu);
+            }
+        };
+        using K0 = std::integral_constant<int, 0>;
+        using K1 = std::integral_constant<int, 1>;
+        using K2 = std::integral_constant<int, 2>;
+        using W0 = std::integral_constant<int, 0>;
+        using W1 = std::integral_constant<int, 1>;
+        using NC = std::false_type;
+        using CR = std::true_type;
+        if (P > 4) {
+            step(X, Y, 0, K0{}, W0{}, NC{});
+            step(Y, X, 1, K1{}, W1{}, NC{});
+        } else {
+            if (has_next)
+                N = geo(i0 + stride);
+            step(X, Y, 0, K0{}, W0{}, CR{});
+            step(Y, X, 1, K1{}, W1{}, CR{});
+        }
+        int j = 2;
+        for (; j + 4 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, NC{});
+            step(Y, X, j + 1, K2{}, W1{}, NC{});
+        }
+        if (has_next)
+            N = geo(i0 + stride);
+        for (; j + 1 < P; j += 2) {
+            step(X, Y, j, K2{}, W0{}, CR{});
+            step(Y, X, j + 1, K2{}, W1{}, CR{});
+        }
+        if (j < P)
+            step(X, Y, j, K2{}, W0{}, CR{});
+        // border rows of the image: first row +1, last row -1 (its down pairs
+        // were emitted as equal fakes: the down row was the row itself)
+        if (__any_sync(0xFFFFFFFFu, G.nrows > 0 && (G.y0 == 0 || G.y0 + G.nrows == p.h))) {
+            const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
+            if (G.nrows > 0 && G.y0 == 0) {
+                const uint8_t* rp = G.p + p.pitch;
+                for (int i = 0; i < nreal; ++i)
+                    red_add(corr_g + ((uint32_t)rp[i] << 2), 1u);
+            }
+            if (G.nrows > 0 && G.y0 + G.nrows == p.h) {
+                const uint8_t* rp = G.p + (size_t)G.nrows * p.pitch;
+                for (int i = 0; i < nreal; ++i)
+                    red_add(corr_g + ((uint32_t)rp[i] << 2), 0xFFFFFFFFu);
+            }
+        }
+        __syncthreads();
+        TWCYC(0);  // walk (incl. the wait for the slowest warp)
+        if (!waited) {
+            pdl_wait();  // the previous launch may still read our outputs
+            waited = true;
+        }
+        if constexpr (LG == 4) {
+            // Cooperative flush for 8 images per round (C5): warp w owns the
+            // keys [16 w, 16 w + 16) of all 8 images; lane L takes image
+            // L & 7, keys t0 .. t0 + 3 (t0 = 16 w + 4 (L >> 3)).  A group's 4
+            // lane words of a counter row are one 16-byte piece, and the 8
+            // lanes of a quarter warp (one LDS.128 wavefront) hit 8 bank quads, so
+            // the counters are read once, conflict free, straight into the
+            // per-image combinations; the scans run across the 4 lanes of an
+            // image and then across warps (two small carry exchanges).  No
+            // transposed scratch copy, no second clearing pass.
+            // (the 8 lanes of each quarter warp -- one LDS.128 wavefront --
+            // take 8 different images, i.e. 8 different bank quads)
+            const int gi = lane & 7, q4 = lane >> 3;
+            const int t0 = 16 * warp + 4 * q4;
+            auto grp = [&](int row, int half) -> uint4 {
+                return *reinterpret_cast<const uint4*>(hist + row * 256 + half * 128 + gi * 16);
+            };
+            auto wsum = [](const uint4& v, long long& h, long long& b) {
+                h += (long long)((v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu));
+                b += (long long)((v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16));
+            };
+            long long hv[5] = {0, 0, 0, 0, 0};  // hist(t0 - 1 + i)
+            long long cd[4], h2[4];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const int t = t0 - 1 + i;
+                long long hh = 0, bb = 0;
+                if (t >= 0) {
+                    wsum(grp(t, 1), hh, bb);        // W copy 0
+                    wsum(grp(256 + t, 1), hh, bb);  // W copy 1
+                }
+                hv[i] = hh;
+                if (i > 0)
+                    cd[i - 1] = bb - 4ll * hh;
+            }
+            long long hs[9];  // Hs rows 2 t0 - 3 .. 2 t0 + 5
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const int r = 2 * t0 - 3 + i;
+                long long v = 0;
+                if (r >= 0) {
+                    const uint4 c = grp(r, 0);
+                    v = (long long)c.x + c.y + c.z + c.w;
+                }
+                hs[i] = v;
+            }
+            const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + gi * 1024);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int u = t0 + i;  // h2(u) = 4 hist(u-1) - corr(u-1) - hs(2u-3) - 2 hs(2u-2) - hs(2u-1)
+                h2[i] = u == 0 ? 0
+                               : 4ll * hv[i] - (long long)cr[u - 1] - hs[2 * i] - 2ll * hs[2 * i + 1] -
+                                     hs[2 * i + 2];
+            }
+            // hs[0] (row 2 t0 - 3) is counted for u = t0 only when u >= 2: a
+            // negative row is 0 already, so the formula matches warp_curve256's
+            uint32_t hist_keep[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                hist_keep[i] = (uint32_t)hv[i + 1];
+            __syncthreads();  // every counter read: clear the block for the next round
+            {
+                uint4* z = reinterpret_cast<uint4*>(hist);
+                for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
+                    z[i] = make_uint4(0, 0, 0, 0);
+            }
+            // scans: lane-local, then across the image's 4 lanes (a quad)
+            long long* tot = reinterpret_cast<long long*>(sm + Lay::kTot);  // [3][16][NG]
+            auto quad_scan = [&](long long (&v)[4]) -> long long {
+#pragma unroll
+                for (int i = 1; i < 4; ++i)
+                    v[i] += v[i - 1];
+                long long x = v[3];  // the image's 4 lanes are gi, gi + 8, gi + 16, gi + 24
+#pragma unroll
+                for (int off = 1; off < 4; off <<= 1) {
+                    const long long y = __shfl_up_sync(0xFFFFFFFFu, x, 8 * off);
+                    if (q4 >= off)
+                        x += y;
+                }
+                const long long ex = x - v[3];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    v[i] += ex;
+                return __shfl_sync(0xFFFFFFFFu, x, 24 + gi);  // the image's (= warp's) total
+            };
+            const long long tc = quad_scan(cd);
+            const long long tg = quad_scan(h2);  // h2 -> g (sum first difference)
+            if (q4 == 0) {
+                tot[(0 * 16 + warp) * NG + gi] = tc;
+                tot[(1 * 16 + warp) * NG + gi] = tg;
+            }
+            __syncthreads();
+            long long cc = 0, cg = 0;
+            for (int w2 = 0; w2 < warp; ++w2) {
+                cc += tot[(0 * 16 + w2) * NG + gi];
+                cg += tot[(1 * 16 + w2) * NG + gi];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cd[i] += cc;  // card
+                h2[i] += cg;  // g
+            }
+            const long long ts = quad_scan(h2);  // g -> sum, without the carry of earlier warps' g
+            if (q4 == 0)
+                tot[(2 * 16 + warp) * NG + gi] = ts;
+            __syncthreads();
+            long long cs = 0;
+            for (int w2 = 0; w2 < warp; ++w2)
+                cs += tot[(2 * 16 + w2) * NG + gi];
+            const long long im = i0 + gi;
+            if (im < p.n) {
+                uint64_t* os = p.sums + (size_t)im * 256 + t0;
+                uint64_t* oc = p.cards + (size_t)im * 256 + t0;
+                *reinterpret_cast<ulonglong2*>(oc) = make_ulonglong2((uint64_t)cd[0], (uint64_t)cd[1]);
+                *reinterpret_cast<ulonglong2*>(oc + 2) = make_ulonglong2((uint64_t)cd[2], (uint64_t)cd[3]);
+                *reinterpret_cast<ulonglong2*>(os) =
+                    make_ulonglong2((uint64_t)(h2[0] + cs), (uint64_t)(h2[1] + cs));
+                *reinterpret_cast<ulonglong2*>(os + 2) =
+                    make_ulonglong2((uint64_t)(h2[2] + cs), (uint64_t)(h2[3] + cs));
+                if (p.hist_out) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        p.hist_out[(size_t)im * 256 + t0 + i] = hist_keep[i];
+                }
+            }
+            TWCYC(1);
+            for (int i = tid; i < NG * 256; i += kTwThreads)
+                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
+        } else
+        {
+            // 1. every thread: 2*NG (half-row, group) cells, contiguous 16-byte
+            //    pieces across a warp (conflict free): read, sum the group's LG
+            //    lane words (fields for W), clear
+            constexpr int PER = 1024 * NG / kTwThreads;
+            uint32_t va[PER], vb[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int idx = tid + kTwThreads * q;
+                const int rh = idx / NG, gg = idx % NG;
+                uint32_t a = 0, b = 0;
+#pragma unroll
+                for (int q4 = 0; q4 < LG / 4; ++q4) {
+                    uint4* cell = reinterpret_cast<uint4*>(hist + rh * 128 + gg * LG * 4 + 16 * q4);
+                    const uint4 v = *cell;
+                    if (rh & 1) {  // W word: hist | B << 16
+                        a += (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
+                        b += (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
+                    } else {
+                        a += v.x + v.y + v.z + v.w;
+                    }
+                    *cell = make_uint4(0, 0, 0, 0);
+                }
+                va[q] = a;
+                vb[q] = b;
+            }
+            __syncthreads();
+            TWCYC(1);
+            // 2. per-image totals into a padded scratch carved out of the (now
+            //    zero) counter block: hs[s] at s + s/16, the other arrays at
+            //    x + x/8 (conflict-free lane-blocked reads of warp_curve256)
+            uint32_t* scr = reinterpret_cast<uint32_t*>(hist);
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int idx = tid + kTwThreads * q;
+                const int rh = idx / NG, gg = idx % NG;
+                const int row = rh >> 1;
+                uint32_t* base = scr + gg * kTwImgWords;
+                if (rh & 1) {
+                    const int key = row & 255, cp = row >> 8;
+                    base[kTwH + cp * 2 * kTwArr + pad8(key)] = va[q];
+                    base[kTwH + cp * 2 * kTwArr + kTwArr + pad8(key)] = vb[q];
+                } else {
+                    base[pad16(row)] = va[q];
+                }
+            }
+            __syncthreads();
+            TWCYC(2);
+            if (warp < NG && i0 + warp < p.n) {
+                // 3. K3 for image i0 + warp
+                const uint32_t* base = scr + warp * kTwImgWords;
+                const uint32_t* h0 = base + kTwH;
+                const uint32_t* b0 = h0 + kTwArr;
+                const uint32_t* h1 = b0 + kTwArr;
+                const uint32_t* b1 = h1 + kTwArr;
+                const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + warp * 1024);
+                auto histv = [&](int v) { return (long long)h0[pad8(v)] + (long long)h1[pad8(v)]; };
+                auto hs = [&](int s) { return (long long)base[pad16(s)]; };
+                uint64_t card[8], sum[8];
+                warp_curve256_regs(
+                    [&](int t) {
+                        return (long long)b0[pad8(t)] + (long long)b1[pad8(t)] - 4ll * histv(t);
+                    },
+                    [&](int u) -> long long {
+                        if (u == 0)
+                            return 0;
+                        long long r2 = 4ll * histv(u - 1) - (long long)cr[u - 1] -
+                                       2ll * hs(2 * u - 2) - hs(2 * u - 1);
+                        if (u >= 2)
+                            r2 -= hs(2 * u - 3);
+                        return r2;
+                    },
+                    card, sum);
+                const long long im = i0 + warp;
+                uint64_t* os = p.sums + (size_t)im * 256 + lane * 8;
+                uint64_t* oc = p.cards + (size_t)im * 256 + lane * 8;
+#pragma unroll
+                for (int jj = 0; jj < 8; jj += 2) {
+                    *reinterpret_cast<ulonglong2*>(os + jj) = make_ulonglong2(sum[jj], sum[jj + 1]);
+                    *reinterpret_cast<ulonglong2*>(oc + jj) = make_ulonglong2(card[jj], card[jj + 1]);
+                }
+                if (p.hist_out) {
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        p.hist_out[(size_t)im * 256 + lane * 8 + jj] = (uint32_t)histv(lane * 8 + jj);
+                }
+            }
+            __syncthreads();
+            TWCYC(3);
+            // 4. clear the scratch and the border terms for the next round
+            uint4* z = reinterpret_cast<uint4*>(hist);
+            for (int i = tid; i < NG * kTwImgWords / 4; i += kTwThreads)
+                z[i] = make_uint4(0, 0, 0, 0);
+            for (int i = tid; i < NG * 256; i += kTwThreads)
+                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
+        }
+        __syncthreads();
+        TWCYC(4);
+        pos += (uint32_t)P;
+        G = N;
+    }
+#ifdef KOHLER_PHASES
+    if (threadIdx.x == 0 && blockIdx.x < 2048)
+        for (int i = 0; i < 5; ++i)
+            g_phase[blockIdx.x][i] = (unsigned long long)tw_acc[i];
+#endif
+#undef TWCYC
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (!waited)
+        pdl_wait();
+    pdl_trigger();
+}
+
+} // namespace
