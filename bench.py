@@ -201,6 +201,11 @@ def main():
     ap.add_argument("--graph-steps", type=int, default=60,
                     help="N=1: replay the step loop from CUDA graphs of this many consecutive "
                          "steps (PDL edges between them inside the graph); 0 = eager launches")
+    ap.add_argument("--eager-bands", action="store_true",
+                    help="N>1 (or --force-bands): launch the band steps eagerly instead of "
+                         "replaying them (NCCL all-reduces included) from CUDA graphs")
+    ap.add_argument("--force-reduce", action="store_true",
+                    help="with --force-bands at N=1: issue the all-reduce anyway (tests)")
     ap.add_argument("--force-bands", action="store_true",
                     help="run the multi-GPU row-band path (NCCL) even at N=1 (launch under "
                          "torchrun; exercises the N>1 code on one GPU, not a scaling number)")
@@ -258,6 +263,7 @@ def main():
                        "(kohler_cuda_set_pipeline_depth)" if args.depth > 1 else ""))
     else:
         ba = BandedAnalyzer(ctx, w, h, world, rank, K_TOP)
+        ba.always_reduce = args.force_reduce
         pitch = (w + 127) // 128 * 128
         rows = ba.rows_held
         band_bytes = max(rows, 1) * pitch
@@ -303,18 +309,23 @@ def main():
     drain()
     torch.cuda.synchronize()
 
-    # N=1: a step is one K1 + one finish launch (~9-15 us of host API time per
-    # step through ctypes, as long as the device step): replay the loop from
-    # CUDA graphs of G consecutive steps, captured through the same public
-    # device API on the capture stream (PDL edges between the steps inside)
+    # A step is a few launches (~9-15 us of host API time per step through
+    # ctypes, as long as the device step): replay the loop from CUDA graphs of
+    # G consecutive steps, captured through the same public device API on the
+    # capture stream (N=1: PDL edges between the steps inside; N>1: the band
+    # kernels, the NCCL all-reduces and the selections with their overlap)
     graph = None
-    G = args.graph_steps if not bands else 0
+    G = args.graph_steps if (not bands or not args.eager_bands) else 0
     if G > 0:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             cap = torch.cuda.current_stream()
             for j in range(G):
-                step(j, cap)
+                if bands:
+                    step(j)
+                else:
+                    step(j, cap)
+            drain()
         graph.replay()
         torch.cuda.synchronize()
 
@@ -341,11 +352,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    if rank == 0 and not bands:
+    if rank == 0:
         # the replayed / pipelined steps left the last image's full result
         ok = int(out["t0"][0]) == exp["t0"] and \
-            out["topk"][: int(out["topk_count"][0])].tolist() == exp["topk"] and \
-            np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"])
+            out["topk"][: int(out["topk_count"][0])].tolist() == exp["topk"]
+        if not bands:
+            ok = ok and np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"])
         if not ok:
             raise SystemExit("timed steps produced a result that differs from the oracle")
     ms = e0.elapsed_time(e1)

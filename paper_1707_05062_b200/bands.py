@@ -47,6 +47,7 @@ class BandedAnalyzer:
         # flight while step i + 1's band accumulates
         self._curves = [torch.zeros(512, dtype=torch.int64, device=dev) for _ in range(2)]
         self._pending = None  # (work handle, buffer) of the previous step
+        self.always_reduce = False  # all-reduce even with one rank (tests of the N > 1 path)
         self.out = {"values": torch.zeros(256, dtype=torch.float64, device=dev),
                     "defined": torch.zeros(256, dtype=torch.uint8, device=dev),
                     "t0": torch.zeros(1, dtype=torch.int32, device=dev),
@@ -66,13 +67,13 @@ class BandedAnalyzer:
         lib = getattr(self.ctx, "_lib", None)
         if lib is None:
             return None
-        if getattr(self, "_fc", None) is None:
+        st = torch.cuda.current_stream()  # the capture stream while a graph is recorded
+        if getattr(self, "_fc", None) is None or self._fc[2] != st.cuda_stream:
             o = self.out
-            st = torch.cuda.current_stream().cuda_stream
             h = self.ctx.handle
             outs = (o["values"].data_ptr(), o["defined"].data_ptr(), o["t0"].data_ptr(),
                     o["topk"].data_ptr(), o["topk_count"].data_ptr(), o["status"].data_ptr())
-            self._fc = (lib, h, st, outs)
+            self._fc = (lib, h, st.cuda_stream, outs)
         return self._fc
 
     def _select(self, curve: torch.Tensor) -> None:
@@ -115,7 +116,8 @@ class BandedAnalyzer:
         else:
             cur.zero_()
         work = None
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if dist.is_available() and dist.is_initialized() and (
+                self.always_reduce or dist.get_world_size(self.group) > 1):
             work = dist.all_reduce(cur, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         self.drain()
         self._pending = (work, cur)
