@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--graph-steps", type=int, default=60,
                     help="N=1: replay the step loop from CUDA graphs of this many consecutive "
                          "steps (PDL edges between them inside the graph); 0 = eager launches")
+    ap.add_argument("--band-depth", type=int, default=1,
+                    help="N>1: pipeline depth of the band kernels (kohler_cuda_set_pipeline_depth)")
     ap.add_argument("--eager-bands", action="store_true",
                     help="N>1 (or --force-bands): launch the band steps eagerly instead of "
                          "replaying them (NCCL all-reduces included) from CUDA graphs")
@@ -264,6 +266,7 @@ def main():
     else:
         ba = BandedAnalyzer(ctx, w, h, world, rank, K_TOP)
         ba.always_reduce = args.force_reduce
+        ctx.set_pipeline_depth(args.band_depth)
         pitch = (w + 127) // 128 * 128
         rows = ba.rows_held
         band_bytes = max(rows, 1) * pitch
