@@ -29,6 +29,12 @@
  *                                   quantize, pass-through without boundary) and, with
  *                                   k >= 1, the segment command's top-k quantize
  *                                   (tools/kohler_main.cpp:91-103)
+ *   kohler_cuda_rgb_to_gray[_device] -> luma601 inside read_pnm for P6 / P3
+ *                                   (src/pnm.cpp:63-68,110-136)
+ *   kohler_cuda_analyze_rgb_batch[_device] -> fast_contrast_curve(read_pnm(P6/P3)) + selection
+ *   kohler_cuda_submit / _collect -> the per-frame loops of src/bench.cpp:264-284 at PCIe
+ *                                   speed (two frames in flight; no reference counterpart)
+ *   kohler_cuda_set_pipeline_depth -> throughput mode for device loops (no counterpart)
  *
  * Results are bit-identical to the reference: integer curves exactly, the
  * double curve bit-for-bit (IEEE division of exactly-representable operands),
