@@ -8,12 +8,19 @@ one pass of that pipeline over the image.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N = 1: one fused launch per step (K1 accumulate + K3 reconstruct + K4 select).
+N = 1: per step one K1 launch (accumulate) and one finish launch (K3
+reconstruct + K4 select), PDL-chained; pipeline depth 3 (three steps in
+flight on a third of the SMs each) and the step loop replayed from CUDA
+graphs of 60 steps captured through the public device API.  e2e: the host C
+ABI with a pinned host image every step (streaming submit/collect, and the
+synchronous call beside it).
 N > 1 (torchrun, one process per GPU, NCCL): the image is split into row
 bands with a one-row halo (proj/src/fast.cpp:42-57); per step each rank runs
-K1 on its band, one all-reduce of the 512 u64 partials, then K4 — strong
-scaling (the image is fixed).  Timing: CUDA events on the launching stream,
-barrier + synchronize on both sides, max over ranks.  L2 (126 MB) is defeated
+K1 on its band, one all-reduce of the 512 u64 partials (overlapped with the
+next step's band), then K4 — strong scaling (the image is fixed); also
+graph-replayed.  Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks; the last step's result is
+re-checked against the oracle after the timed loop.  L2 (126 MB) is defeated
 by rotating through input copies totalling > 2x L2.
 
 `--impl reference` times the reference's own CPU implementation
