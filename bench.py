@@ -327,17 +327,25 @@ def main():
     graph = None
     G = args.graph_steps if (not bands or not args.eager_bands) else 0
     if G > 0:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            cap = torch.cuda.current_stream()
-            for j in range(G):
-                if bands:
-                    step(j)
-                else:
-                    step(j, cap)
-            drain()
-        graph.replay()
-        torch.cuda.synchronize()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cap = torch.cuda.current_stream()
+                for j in range(G):
+                    if bands:
+                        step(j)
+                    else:
+                        step(j, cap)
+                drain()
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # keep a (slower, eager) bench line rather than none
+            print(f"bench: CUDA-graph capture failed ({type(exc).__name__}: {exc}); eager steps",
+                  file=sys.stderr, flush=True)
+            graph = None
+            torch.cuda.synchronize()
+            if bands:
+                ba._pending = None
 
     sampler = ClockSampler(dev.index if world == 1 else local).start()
     sampler.wait_first()
