@@ -382,7 +382,9 @@ __device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint3
 {
     asm volatile(
         "{\n\t.reg .pred pl, pr;\n\tsetp.ne.u32 pl, %2, 0;\n\tsetp.ne.u32 pr, %3, 0;\n\t"
+#ifndef KOHLER_PROBE_NO_ROWLOADS
         "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
+#endif
 #ifndef KOHLER_PROBE_NO_PADS
         "@pl cp.async.cg.shared.global [%0+512], [%1+-16], 16;\n\t"
         "@pr cp.async.cg.shared.global [%0+32], [%1+16], 16;\n\t"
