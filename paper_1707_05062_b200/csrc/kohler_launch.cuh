@@ -475,10 +475,14 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     const size_t n256 = (size_t)n * 256;
     const size_t tail_off = round_up(n256 * 25, 16);
     const size_t bytes = tail_off + (size_t)n * 4 * 3 + (size_t)n * k * 4;
-    rc = ctx->out.ensure(bytes + 64);
+    // small results (<= 64 KiB): the kernels write them straight into the
+    // pinned host staging block (mapped, unified addressing), so no separate
+    // device-to-host copy sits at the end of the call
+    const bool small = bytes <= (64u << 10);
+    rc = small ? ctx->hout.ensure(bytes + 64) : ctx->out.ensure(bytes + 64);
     if (rc)
         return rc;
-    char* b = static_cast<char*>(ctx->out.p);
+    char* b = static_cast<char*>(small ? ctx->hout.p : ctx->out.p);
     BatchOut d{};
     const bool want_curve = true;  // curves always land in the packed block
     d.sums = want_curve ? reinterpret_cast<uint64_t*>(b) : nullptr;
@@ -572,12 +576,8 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
         if (rc)
             return rc;
     }
-    if (bytes <= (64u << 10)) {
-        // one packed copy back, then scatter on the host
-        rc = ctx->hout.ensure(bytes);
-        if (rc)
-            return rc;
-        KC_CUDA(cudaMemcpyAsync(ctx->hout.p, b, bytes, cudaMemcpyDeviceToHost, st));
+    if (small) {
+        // the results are already in the pinned block: wait, then scatter
         KC_CUDA(cudaStreamSynchronize(st));
         const char* hb = static_cast<const char*>(ctx->hout.p);
         if (host.sums)
