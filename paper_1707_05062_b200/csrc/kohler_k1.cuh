@@ -174,6 +174,16 @@ __device__ __forceinline__ void border_prefetch(const WideParams& p, int img, co
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+template <bool RGB>
+__device__ __forceinline__ int border_px(const uint8_t* row, int x)
+{
+    if constexpr (RGB)
+        return (int)luma1(row[3 * x], row[3 * x + 1], row[3 * x + 2]);
+    else
+        return row[x];
+}
+
+template <bool RGB>
 __device__ __forceinline__ void border_pass(const WideParams& p, int img, const BorderSlice& s,
                                             const uint8_t* pre, uint32_t* hb, int* corr_tot)
 {
@@ -186,14 +196,14 @@ __device__ __forceinline__ void border_pass(const WideParams& p, int img, const 
     KCYC(0);
     for (int x = s.xa + (int)threadIdx.x; x < s.xb; x += kWalkThreads) {
         const int o = x - 16 * s.ca;
-        const int v0 = pre ? pre[o] : base[x];
-        const int c = pre ? pre[kBorderRow + o] : rl[x];
+        const int v0 = pre ? pre[o] : border_px<RGB>(base, x);
+        const int c = pre ? pre[kBorderRow + o] : border_px<RGB>(rl, x);
         KCYC(1);
         atomicAdd(&corr_tot[v0], 1);
         if (img_last) {
             atomicAdd(&corr_tot[c], -1);
         } else {
-            const int d = pre ? pre[2 * kBorderRow + o] : rl[p.pitch + x];
+            const int d = pre ? pre[2 * kBorderRow + o] : border_px<RGB>(rl + p.pitch, x);
             atomicAdd(&hb[d], 1u);
             atomicAdd(&hb[256 + d], (uint32_t)(4 + (c > d) - (c < d)));
             atomicAdd(&corr_tot[d], 3);
@@ -206,6 +216,7 @@ __device__ __forceinline__ void border_pass(const WideParams& p, int img, const 
 // CTA flush of one image's partial: reduce the striped counters (clearing
 // them for the next image), form the 512 combinations, REDG them into the
 // image's accumulator (finish_kernel takes it from there).
+template <bool RGB>
 __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, unsigned char* hist,
                             bool clear, bool two_w, bool prefetched, bool first)
 {
@@ -239,7 +250,7 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
     KCYC(4);
     // the first image's slice was computed at kernel start (gridDim / params
     // are cold in the constant cache by now)
-    border_pass(p, img, first ? *reinterpret_cast<const BorderSlice*>(sm + kSmBslice) : border_slice(p, img),
+    border_pass<RGB>(p, img, first ? *reinterpret_cast<const BorderSlice*>(sm + kSmBslice) : border_slice(p, img),
                 prefetched ? sm + kSmBorder : nullptr, hb, corr_tot);
     KCYC(5);
     __syncthreads();
@@ -307,9 +318,11 @@ struct LaneGeo {
     int jlo, jcl;      // ring position j loads row y0 - 1 + clamp(j, jlo, jcl)
 };
 
+template <bool RGB>
 __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* base, long long g,
                                             int lane)
 {
+    using F = K1Fmt<RGB>;
     LaneGeo L;
     const unsigned long long tau = (unsigned long long)g * 32ull + (unsigned)lane;
     const bool act = tau < (unsigned long long)p.T;
@@ -330,9 +343,9 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
         L.jlo = 0;
         L.jcl = 0;
     }
-    L.p = base + ((long long)L.y0 - 1) * (long long)p.pitch + L.x0;
-    L.pd = lane == 0 ? -16 : 16;
-    L.pds = lane == 0 ? 512 : 528 - 16 * 31;
+    L.p = base + ((long long)L.y0 - 1) * (long long)p.pitch + (long long)L.x0 * F::bpp;
+    L.pd = lane == 0 ? -16 : (int)F::seg;
+    L.pds = lane == 0 ? (int)F::lpad : (int)(F::rpad - F::seg * 31);
     L.pad = ((lane == 0) & (L.x0 > 0)) | ((lane == 31) & (L.e > 15)) ? 1u : 0u;
     return L;
 }
@@ -341,10 +354,23 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
 // (shared address of this lane's 16-byte segment in the slot): the segment,
 // from a clamped valid row, and for lane 0 / lane 31 the 16 bytes left /
 // right of it where that neighbour exists.  One cp.async group per position.
+template <bool RGB>
 __device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitch, uint32_t dst)
 {
     const uint32_t off = (uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
     const uint8_t* src = L.p + off;
+    if constexpr (RGB) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+            "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
+            "cp.async.cg.shared.global [%0+16], [%1+16], 16;\n\t"
+            "cp.async.cg.shared.global [%0+32], [%1+32], 16;\n\t"
+            "@p cp.async.cg.shared.global [%3], [%4], 16;\n\t"
+            "cp.async.commit_group;\n\t}" ::"r"(dst),
+            "l"(src), "r"(L.pad), "r"(dst + L.pds), "l"(src + L.pd)
+            : "memory");
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
         "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
@@ -378,8 +404,26 @@ __device__ __forceinline__ FetchStream fetch_stream(const LaneGeo& L, int j, uin
     return f;
 }
 
+template <bool RGB>
 __device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint32_t dst)
 {
+    if constexpr (RGB) {
+        // segment = 3 chunks; left pad: slot + lpad <- src - 16 (lane 0 at
+        // slot + 0); right pad: slot + rpad = lane 31's segment + 64 <- src + 48
+        asm volatile(
+            "{\n\t.reg .pred pl, pr;\n\tsetp.ne.u32 pl, %2, 0;\n\tsetp.ne.u32 pr, %3, 0;\n\t"
+            "cp.async.cg.shared.global [%0], [%1], 16;\n\t"
+            "cp.async.cg.shared.global [%0+16], [%1+16], 16;\n\t"
+            "cp.async.cg.shared.global [%0+32], [%1+32], 16;\n\t"
+            "@pl cp.async.cg.shared.global [%0+1536], [%1+-16], 16;\n\t"
+            "@pr cp.async.cg.shared.global [%0+64], [%1+48], 16;\n\t"
+            "cp.async.commit_group;\n\t}" ::"r"(dst),
+            "l"(f.src), "r"(f.pl), "r"(f.pr)
+            : "memory");
+        f.src += f.left > 0 ? pitch : 0u;
+        --f.left;
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred pl, pr;\n\tsetp.ne.u32 pl, %2, 0;\n\tsetp.ne.u32 pr, %3, 0;\n\t"
 #ifndef KOHLER_PROBE_NO_ROWLOADS
@@ -403,24 +447,50 @@ __device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint3
 // the pad byte (first lane of a run, not at a row start) or the previous
 // lane's last byte; the right one likewise (row end / last lane / next lane).
 struct NbrSel {
-    uint32_t pad_off;  // shared offset of this lane's pad byte from its segment (if any)
+    uint32_t pad_off;  // shared offset of this lane's pad byte (RGB: word) from its segment
+    uint32_t pad_sh;   // RGB: right shift of the pad word to its pixel's bytes
     bool pad;          // lane reads a pad byte
     bool l_own, l_pad;
     bool r_own, r_pad;
 };
 
+template <bool RGB>
 __device__ __forceinline__ void read_row_shfl(kohler_walk::Row& r, uint32_t seg, const NbrSel& n)
 {
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
-                 : "r"(seg)
-                 : "memory");
     uint32_t pb = 0;
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
-                 "@p ld.shared.u8 %0, [%2];\n\t}"
-                 : "+r"(pb)
-                 : "r"((uint32_t)n.pad), "r"(seg + n.pad_off)
-                 : "memory");
+    if constexpr (RGB) {
+        // 48 bytes of interleaved RGB -> 16 luma bytes (the reference's luma601);
+        // the pad pixel's three bytes are one aligned word (lane 0: bytes 1..3
+        // of the left pad's last word; lane 31: bytes 0..2 of the right pad)
+        uint32_t c[12];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(c[4 * q]), "=r"(c[4 * q + 1]), "=r"(c[4 * q + 2]), "=r"(c[4 * q + 3])
+                         : "r"(seg + 16u * q)
+                         : "memory");
+        uint32_t pw = 0;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+                     "@p ld.shared.u32 %0, [%2];\n\t}"
+                     : "+r"(pw)
+                     : "r"((uint32_t)n.pad), "r"(seg + n.pad_off)
+                     : "memory");
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            r.w[j] = luma4(c[3 * j], c[3 * j + 1], c[3 * j + 2]);
+        pw >>= n.pad_sh;
+        pb = luma_div(__dp2a_hi(114u, pw, __dp2a_lo(299u | 587u << 16, pw, 500u)));
+    } else {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                     : "r"(seg)
+                     : "memory");
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+                     "@p ld.shared.u8 %0, [%2];\n\t}"
+                     : "+r"(pb)
+                     : "r"((uint32_t)n.pad), "r"(seg + n.pad_off)
+                     : "memory");
+    }
     const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, r.w[3], 1);
     const uint32_t dn = __shfl_down_sync(0xFFFFFFFFu, r.w[0], 1);
     r.ln = n.l_own ? (r.w[0] & 0xFFu) : n.l_pad ? pb : (up >> 24);
@@ -447,7 +517,7 @@ __device__ __forceinline__ GroupFlags group_flags(const LaneGeo& L, bool aligned
 // segments (one per group touched); a segment of L rows is L + 2 ring
 // positions: row r0 - 1 (absorbed), row r0 (prime: q of the up pairs), then
 // one position per row.  Rows stream through the warp's 4-slot shared ring,
-// prefetched 3 positions ahead across segment boundaries.  The W copy
+// prefetched 3 positions ahead (RGB: 2) across segment boundaries.  The W copy
 // alternates with the position parity (bounds each copy's events).
 // Clear the counter block (one W copy: rows 256..511 only have their Hs half
 // in use) and the per-CTA scratch.
@@ -473,7 +543,7 @@ __device__ __forceinline__ void zero_counters(unsigned char* sm, unsigned char* 
         reinterpret_cast<uint32_t*>(sm + kSmHb)[i] = 0;
 }
 
-template <bool ALIGNED, bool TWO_W>
+template <bool ALIGNED, bool TWO_W, bool RGB>
 __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
                                            unsigned char* hist, uint32_t smbase,
                                            const uint8_t* base, long long ua, long long ub,
@@ -483,16 +553,19 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane4 = (uint32_t)lane * 4u;
-    const uint32_t kneg = kHistAbs - lane4;  // pair event at A_a + A_b + kneg
-    const uint32_t dummy = kHistAbs + kDummy + lane4;
+    using F = K1Fmt<RGB>;
+    constexpr uint32_t HA = F::hist_abs;
+    const uint32_t kneg = HA - lane4;  // pair event at A_a + A_b + kneg
+    const uint32_t dummy = HA + kDummy + lane4;
     // corr[v] of a pixel with W address A: corr_base + (A >> 6) (A >> 6 = 4v + (lane4 >> 6))
-    const uint32_t corr_base = smbase + kSmCorr - (lane4 >> 6);
+    const uint32_t corr_base = smbase + F::shift + kSmCorr - (lane4 >> 6);
     const int R = p.R;
     const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
     const bool any = ua < ub;
     // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
     const uint32_t ring = (smbase + kSmRing + 127u) & ~127u;
-    const uint32_t seg0 = ring + (uint32_t)warp * (kRingSlots * kSlotBytes) + (uint32_t)lane * 16u;
+    constexpr int AH = F::ahead;  // positions in flight (ring slots - 1)
+    const uint32_t seg0 = ring + (uint32_t)warp * (F::slots * F::slot) + (uint32_t)lane * F::seg;
 
     // current segment: group g, rows [r0, r1) of its walks; next segment
     long long g = 0;
@@ -502,11 +575,12 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         g = ua / R;
         r0 = (int)(ua - g * R);
         r1 = (int)(ub - g * R < (long long)R ? (int)(ub - g * R) : R);
-        G = lane_geo(p, base, g, lane);
+        G = lane_geo<RGB>(p, base, g, lane);
         // positions 0, 1, 2 of the first segment (rows r0 - 1, r0, r0 + 1 of the walk)
-        fetch_row(G, r0, pitch, seg0);
-        fetch_row(G, r0 + 1, pitch, seg0 + kSlotBytes);
-        fetch_row(G, r0 + 2, pitch, seg0 + 2 * kSlotBytes);
+        fetch_row<RGB>(G, r0, pitch, seg0);
+        fetch_row<RGB>(G, r0 + 1, pitch, seg0 + F::slot);
+        if (AH > 2)
+            fetch_row<RGB>(G, r0 + 2, pitch, seg0 + 2 * F::slot);
     }
     if (zero_first) {
         // clear the counters while the first rows are in flight
@@ -522,16 +596,16 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     Car X, Y;
     // ring slots of the current position and of the previous one (which the
     // current step refills: (q + 3) & 3 == (q - 1) & 3)
-    const uint32_t slot_end = seg0 + kRingSlots * kSlotBytes;
-    uint32_t sl_cur = seg0, sl_prev = seg0 + (kRingSlots - 1) * kSlotBytes;
+    const uint32_t slot_end = seg0 + F::slots * F::slot;
+    uint32_t sl_cur = seg0, sl_prev = seg0 + (F::slots - 1) * F::slot;
     for (;;) {
         const int L = r1 - r0;
         const int P = L + 2;
-        FetchStream fs = fetch_stream(G, r0 + 3, pitch, lane);
+        FetchStream fs = fetch_stream(G, r0 + AH, pitch, lane);
         const long long gn = g + 1;
         const bool has_next = gn * R < ub;
         const int nr1 = has_next ? (int)(ub - gn * R < (long long)R ? (int)(ub - gn * R) : R) : 0;
-        const LaneGeo N = has_next ? lane_geo(p, base, gn, lane) : G;
+        const LaneGeo N = has_next ? lane_geo<RGB>(p, base, gn, lane) : G;
         const GroupFlags F = group_flags(G, ALIGNED);
         const bool row_start = G.x0 == 0, row_end = G.e <= 15;
         // neighbour bytes: the adjacent lane's segment, lanes 0 / 31 their pad,
@@ -542,7 +616,9 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         nb.r_own = G.e <= 15;
         nb.r_pad = !nb.r_own && lane == 31;
         nb.pad = nb.l_pad || nb.r_pad;
-        nb.pad_off = lane == 0 ? 512u + 15u : 528u - 16u * 31u;
+        nb.pad_off = RGB ? (lane == 0 ? F::lpad + 12u : F::rpad - F::seg * 31u)
+                         : (lane == 0 ? F::lpad + 15u : F::rpad - F::seg * 31u);
+        nb.pad_sh = lane == 0 ? 8u : 0u;
 
         // One ring position j: prefetch position j + 3 (of this segment or,
         // past its end, of the next), absorb row r0 - 1 + j into D and
@@ -553,21 +629,24 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             constexpr int WC = decltype(wc)::value;
             constexpr uint32_t kOffW = (WC && TWO_W) ? kOffW1 : kOffW0;
             // slot q & 3 was committed 3 groups ago; <= 2 younger groups may pend
-            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            if (AH > 2)
+                asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
             // all lanes' copies into slot q & 3 are visible, and all lanes have
             // read slot (q - 1) & 3 (the previous position), which is refilled now
             __syncwarp();
             // read this position's row first: the prefetch issue below
             // covers the LDS latency before the unpack needs the data
             Row r;
-            read_row_shfl(r, sl_cur, nb);
+            read_row_shfl<RGB>(r, sl_cur, nb);
             const uint32_t pref = sl_prev;
             sl_prev = sl_cur;
-            sl_cur = sl_cur + kSlotBytes == slot_end ? seg0 : sl_cur + kSlotBytes;
-            if (!CROSS || j + 3 < P)
-                fetch_next(fs, pitch, pref);
+            sl_cur = sl_cur + F::slot == slot_end ? seg0 : sl_cur + F::slot;
+            if (!CROSS || j + AH < P)
+                fetch_next<RGB>(fs, pitch, pref);
             else if (has_next)
-                fetch_row(N, j + 3 - P, pitch, pref);
+                fetch_row<RGB>(N, j + AH - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
             absorb<ALIGNED>(D, r, lane4, G.e);
@@ -596,7 +675,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 if (live) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        red_add_imm<kHistAbs + kOffW>(C.A[i], b_of(Be, Bo, i));
+                        red_add_imm<HA + kOffW>(C.A[i], b_of(Be, Bo, i));
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
                         red_inc(C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg);
@@ -609,7 +688,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const bool real = i <= G.e;
-                    red_add_imm<kHistAbs + kOffW>(C.A[i], real ? b_of(Be, Bo, i) : 0u);
+                    red_add_imm<HA + kOffW>(C.A[i], real ? b_of(Be, Bo, i) : 0u);
                     red_inc(real ? C.A[i] + (i < 15 ? C.A[i + 1] : Arn) + kneg : dummy);
                     red_inc(real ? C.A[i] + D.A[i] + kneg : dummy);
                 }
@@ -629,7 +708,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
         using NC = std::false_type;
         using CR = std::true_type;
         // positions whose prefetch stays in this segment: j + 3 < P
-        if (P > 4) {
+        if (P > AH + 1) {
             step(X, Y, 0, K0{}, W0{}, NC{});
             step(Y, X, 1, K1{}, W1{}, NC{});
         } else {
@@ -637,7 +716,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
             step(Y, X, 1, K1{}, W1{}, CR{});
         }
         int j = 2;
-        for (; j + 4 < P; j += 2) {
+        for (; j + AH + 1 < P; j += 2) {
             step(X, Y, j, K2{}, W0{}, NC{});
             step(Y, X, j + 1, K2{}, W1{}, NC{});
         }
@@ -657,14 +736,18 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <bool ALIGNED, bool TWO_W>
+template <bool ALIGNED, bool TWO_W, bool RGB>
 __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_constant__ WideParams p)
 {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm);
-    if (smbase + kSmMiscEnd > kHistAbs)
+    using F = K1Fmt<RGB>;
+    extern __shared__ __align__(16) unsigned char sm_dyn[];
+    const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm_dyn);
+    if (smbase + F::shift + kSmMiscEnd > F::hist_abs ||
+        F::hist_abs + kohler_walk::kHistBytes > smbase + F::smem)
         __trap();  // the fixed counter address would overlap the scratch (never seen)
-    unsigned char* hist = sm + (kHistAbs - smbase);
+    unsigned char* hist = sm_dyn + (F::hist_abs - smbase);
+    // the scratch block (all kSm* offsets below), above the ring
+    unsigned char* sm = sm_dyn + F::shift;
     const int tid = threadIdx.x;
     static_assert(sizeof(WideParams) <= 256 && sizeof(WideParams) % 4 == 0, "params copy");
     if (tid < (int)(sizeof(WideParams) / 4))  // read back after the zeroing barrier
@@ -695,9 +778,10 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
         const BorderSlice bs = border_slice(p, i_first);
         if (tid == 0)
             *reinterpret_cast<BorderSlice*>(sm + kSmBslice) = bs;
-        const bool prefetched = bs.xb - bs.xa <= kBorderPx;
+        // (RGB: the border pass reads its rows from global memory)
+        const bool prefetched = !RGB && bs.xb - bs.xa <= kBorderPx;
         if (prefetched)
-            border_prefetch(p, i_first, bs, smbase + kSmBorder);
+            border_prefetch(p, i_first, bs, smbase + F::shift + kSmBorder);
         for (int img = i_first; img <= i_last; ++img) {
             const long long ibase = (long long)img * p.upi;
             const long long a = (cs > ibase ? cs : ibase) - ibase;
@@ -708,7 +792,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
                 const long long n = eb - ea;
                 const long long wa = ea + n * warp / kWalkWarps;
                 const long long wb = ea + n * (warp + 1) / kWalkWarps;
-                walk_range<ALIGNED, TWO_W>(p, sm, hist, smbase, base, wa, wb, !zeroed);
+                walk_range<ALIGNED, TWO_W, RGB>(p, sm, hist, smbase, base, wa, wb, !zeroed);
                 warp_end();
                 zeroed = true;
                 __syncthreads();
@@ -723,7 +807,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
                 pdl_trigger();  // the next launch may start as SMs free up
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");  // border words (walk-less threads)
-            flush_image(ps, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first, img == i_first);
+            flush_image<RGB>(ps, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first, img == i_first);
             // (the last image: no re-zeroing)
             flushed = true;
         }

@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
     const long long stride = (long long)gridDim.x * NG;
     long long i0 = (long long)blockIdx.x * NG;
     LaneGeo G = geo(i0);
-    fetch_row(G, 0, pitch, seg0);
-    fetch_row(G, 1, pitch, seg0 + Lay::kSlot);
-    fetch_row(G, 2, pitch, seg0 + 2 * Lay::kSlot);
+    fetch_row<false>(G, 0, pitch, seg0);
+    fetch_row<false>(G, 1, pitch, seg0 + Lay::kSlot);
+    fetch_row<false>(G, 2, pitch, seg0 + 2 * Lay::kSlot);
     {
         uint4* z = reinterpret_cast<uint4*>(hist);
         for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
@@ -152,12 +152,12 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             __syncwarp();
             Row r;  // read first: the prefetch issue covers the LDS latency
-            read_row_shfl(r, seg0 + (q & 3u) * Lay::kSlot, nb);
+            read_row_shfl<false>(r, seg0 + (q & 3u) * Lay::kSlot, nb);
             const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
             if (!CROSS || j + 3 < P)
-                fetch_row(G, j + 3, pitch, pref);
+                fetch_row<false>(G, j + 3, pitch, pref);
             else if (has_next)
-                fetch_row(N, j + 3 - P, pitch, pref);
+                fetch_row<false>(N, j + 3 - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
             absorb<ALIGNED>(D, r, lane4, G.e);

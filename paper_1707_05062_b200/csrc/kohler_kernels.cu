@@ -130,6 +130,34 @@ static_assert(kSmFinishEnd <= kRingBytes, "finish scratch aliases the ring");
 // the kernel checks kSmMiscEnd fits under kHistAbs
 constexpr uint32_t kSmWideBytes = kHistAbs + kohler_walk::kHistBytes;
 static_assert(kSmWideBytes <= 227 * 1024, "K1 shared memory");
+// K1 over interleaved RGB (colour ingest fused into the walk, SURVEY.md §8f
+// rank 3): a lane segment is 48 bytes (16 pixels), so the ring slots triple;
+// the scratch block moves up by the ring's growth (kRgbShift) and the
+// counter block sits at kHistAbsRgb, whose end is the 227 KiB opt-in limit
+// for any dynamic base <= 1 KiB (the kernel checks both ends).
+constexpr uint32_t kSlotBytesRgb = 1664;  // 32 x 48 B, left pad, right pad, 128-byte multiple
+constexpr int kRingSlotsRgb = 3;          // 2 positions in flight (3 x 1.5 KiB per warp)
+constexpr uint32_t kRingBytesRgb = kWalkWarps * kRingSlotsRgb * kSlotBytesRgb + 128;
+constexpr uint32_t kRgbShift = kRingBytesRgb - kRingBytes;
+constexpr uint32_t kHistAbsRgb = 0x18C00;
+constexpr uint32_t kSmWideBytesRgb = 227 * 1024;
+static_assert(kRgbShift + kSmMiscEnd + 1024 <= kHistAbsRgb, "K1 RGB scratch under the counters");
+static_assert(kHistAbsRgb + kohler_walk::kHistBytes <= kSmWideBytesRgb + 1024, "K1 RGB shared memory");
+
+// Per-input-format constants of K1 (gray: 1 byte per pixel; RGB: 3).
+template <bool RGB>
+struct K1Fmt {
+    static constexpr uint32_t bpp = RGB ? 3 : 1;
+    static constexpr uint32_t seg = 16 * bpp;              // bytes of a lane segment
+    static constexpr uint32_t slot = RGB ? kSlotBytesRgb : kSlotBytes;
+    static constexpr int slots = RGB ? kRingSlotsRgb : kRingSlots;
+    static constexpr int ahead = slots - 1;
+    static constexpr uint32_t lpad = 32 * seg;             // left pad (lane 0) in a slot
+    static constexpr uint32_t rpad = 32 * seg + 16;        // right pad (lane 31)
+    static constexpr uint32_t shift = RGB ? kRgbShift : 0; // scratch offset from the gray map
+    static constexpr uint32_t hist_abs = RGB ? kHistAbsRgb : kHistAbs;
+    static constexpr uint32_t smem = RGB ? kSmWideBytesRgb : kSmWideBytes;
+};
 
 // CTA owning unit u under the balanced partition (first cta_r CTAs hold
 // cta_q + 1 units, the rest cta_q).
@@ -189,6 +217,7 @@ __device__ __forceinline__ void warp_end() {}
 
 } // namespace
 
+#include "kohler_luma.cuh"  // luma4 / luma_div, also used by K1 over RGB
 #include "kohler_k1.cuh"
 #include "kohler_k5.cuh"
 #include "kohler_select.cuh"
@@ -244,8 +273,6 @@ struct HostBuf {
 };
 
 } // namespace
-
-#include "kohler_luma.cuh"
 
 namespace {
 
@@ -310,6 +337,7 @@ struct kohler_cuda_ctx {
     int last_launches = 0;
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
     int depth = 1;      // K1 launches in flight (kohler_cuda_set_pipeline_depth)
+    bool rgb_fused = true;  // K1 reads RGB itself where the layout allows (env KOHLER_RGB_UNFUSED=1: off)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };
@@ -343,6 +371,10 @@ int kohler_cuda_create(int device, kohler_cuda_ctx** out)
                                            std::to_string(major) + std::to_string(minor));
     auto* ctx = new kohler_cuda_ctx();
     ctx->device = device;
+    {
+        const char* e = std::getenv("KOHLER_RGB_UNFUSED");
+        ctx->rgb_fused = !(e && e[0] && e[0] != '0');
+    }
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess)
@@ -711,17 +743,20 @@ int kohler_cuda_analyze_rgb_batch_device(kohler_cuda_ctx* ctx, const uint8_t* rg
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     ctx->last_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
+    const bool select = t0s || topks || topk_counts || status;
+    if (rgb_fused_ok(ctx, rgb, n, w, h, rgb_pitch, rgb_stride))  // one pass: K1 computes the luma
+        return launch_wide(ctx, rgb, n, w, h, h, 0, rgb_pitch, rgb_stride, k, select ? 1 : 0, o, st,
+                           0, nullptr, true);
     const size_t dp = round_up((size_t)w, 16), ds = dp * (size_t)h;
     rc = ctx->gray.ensure(ds * (size_t)n);
     if (rc)
         return rc;
     uint8_t* dg = static_cast<uint8_t*>(ctx->gray.p);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     rc = launch_luma(ctx, rgb, n, w, h, rgb_pitch, rgb_stride, dg, dp, ds, st);
     if (rc)
         return rc;
-    BatchOut o{sums, cards, values, defined, t0s, topks, topk_counts, status};
-    const bool select = t0s || topks || topk_counts || status;
     if (use_tile(n, w, h))
         return launch_tile(ctx, dg, n, w, h, dp, ds, k, select ? 1 : 0, o, st);
     return launch_wide(ctx, dg, n, w, h, h, 0, dp, ds, k, select ? 1 : 0, o, st);

@@ -73,6 +73,17 @@ int check_rgb(int n, int w, int h, size_t pitch, size_t stride)
     return KOHLER_OK;
 }
 
+// K1 over RGB directly (no grey image): whole 16-pixel segments, 16-byte
+// aligned rows and images, and an image large enough for K1 (small images
+// go through luma_kernel + K5)
+bool use_tile(int n, int w, int h);
+bool rgb_fused_ok(const kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, int h, size_t pitch,
+                  size_t stride)
+{
+    return ctx->rgb_fused && w % 16 == 0 && reinterpret_cast<uintptr_t>(rgb) % 16 == 0 &&
+           pitch % 16 == 0 && (n == 1 || stride % 16 == 0) && !use_tile(n, w, h);
+}
+
 int check_image(int n, int w, int h, size_t pitch)
 {
     if (n < 0)
@@ -110,10 +121,12 @@ constexpr bool kSingleW = KOHLER_SINGLE_W != 0;
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
                 const BatchOut& o, cudaStream_t stream, int no_finish = 0,
-                uint32_t* hist_out = nullptr)
+                uint32_t* hist_out = nullptr, bool rgb = false)
 {
     if (n == 0)
         return KOHLER_OK;
+    // rgb: px is interleaved RGB (3 bytes per pixel) and K1 computes the
+    // luma itself; the caller guarantees rgb_fused_ok()
     if (pitch >= (1ull << 31) / 64)
         return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
     const int nseg = (w + 15) / 16;
@@ -217,6 +230,8 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
 
     const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
                      (n == 1 || image_stride % 16 == 0);
+    if (rgb && (!vec || w % 16 != 0 || hist_out))
+        return fail(KOHLER_INVALID_ARGUMENT, "K1 over RGB needs 16-byte aligned rows of whole segments");
     if (!vec) {
         // K1 reads 16-byte segments with cp.async: stage unaligned inputs
         const size_t dpitch = round_up((size_t)w, 16);
@@ -240,33 +255,40 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     }
     // the smem opt-in is per device; remember it per context
     if (!ctx->wide_attr_set) {
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, true>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, true, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, false>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
-        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, false>,
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, false, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytesRgb));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytesRgb));
         ctx->wide_attr_set = true;
     }
     ctx->last_grid = (int)G;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)G);
     cfg.blockDim = dim3(kWalkThreads);
-    cfg.dynamicSmemBytes = kSmWideBytes;
+    cfg.dynamicSmemBytes = rgb ? kSmWideBytesRgb : kSmWideBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (w % 16 == 0)
-        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true>, p)
-                      : cudaLaunchKernelEx(&cfg, walk_kernel<true, false>, p));
+    if (rgb)
+        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true, true>, p)
+                      : cudaLaunchKernelEx(&cfg, walk_kernel<true, false, true>, p));
+    else if (w % 16 == 0)
+        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true, false>, p)
+                      : cudaLaunchKernelEx(&cfg, walk_kernel<true, false, false>, p));
     else
-        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<false, true>, p)
-                      : cudaLaunchKernelEx(&cfg, walk_kernel<false, false>, p));
+        KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<false, true, false>, p)
+                      : cudaLaunchKernelEx(&cfg, walk_kernel<false, false, false>, p));
     ctx->last_launches += 1;
     if (!no_finish) {
         FinishParams fp{};
