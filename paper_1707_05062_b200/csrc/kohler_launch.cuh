@@ -492,6 +492,8 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
             return rc;
     }
     uint8_t* dup = channels == 1 ? dimg : static_cast<uint8_t*>(ctx->rgb.p);
+    // RGB on the 16-pixel grid: K1 walks the uploaded RGB rows itself
+    const bool fused = channels == 3 && rgb_fused_ok(ctx, dup, n, w, h, upitch, ustride);
     cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     // device outputs, packed: sums | cards | values | defined | t0 | count | status | topk
     const size_t n256 = (size_t)n * 256;
@@ -538,7 +540,7 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
         return KOHLER_OK;
     };
     auto to_gray = [&](int i0, int i1, int y0, int y1) -> int {
-        if (channels == 1)
+        if (channels == 1 || fused)
             return KOHLER_OK;
         return launch_luma(ctx, dup + (size_t)i0 * ustride + (size_t)y0 * upitch, i1 - i0, w,
                            y1 - y0, upitch, ustride, dimg + (size_t)i0 * dstride + (size_t)y0 * dpitch,
@@ -578,8 +580,10 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
             rc = to_gray(0, 1, a, std::min(e + 1, h));
             if (rc)
                 return rc;
-            rc = launch_wide(ctx, dimg + (size_t)a * dpitch, 1, w, e - a, h, a, dpitch, dstride, k,
-                             select, d, st, c + 1 < chunks ? 1 : 0);
+            rc = fused ? launch_wide(ctx, dup + (size_t)a * upitch, 1, w, e - a, h, a, upitch, ustride,
+                                     k, select, d, st, c + 1 < chunks ? 1 : 0, nullptr, true)
+                       : launch_wide(ctx, dimg + (size_t)a * dpitch, 1, w, e - a, h, a, dpitch,
+                                     dstride, k, select, d, st, c + 1 < chunks ? 1 : 0);
         } else {
             const int i0 = bound[c], i1 = bound[c + 1];
             rc = upload(i0, i1, 0, h);
@@ -591,7 +595,11 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
             if (rc)
                 return rc;
             const uint8_t* src = dimg + (size_t)i0 * dstride;
-            rc = tile ? launch_tile(ctx, src, i1 - i0, w, h, dpitch, dstride, k, select, sub(i0), st)
+            if (fused)
+                rc = launch_wide(ctx, dup + (size_t)i0 * ustride, i1 - i0, w, h, h, 0, upitch, ustride,
+                                 k, select, sub(i0), st, 0, nullptr, true);
+            else
+                rc = tile ? launch_tile(ctx, src, i1 - i0, w, h, dpitch, dstride, k, select, sub(i0), st)
                       : launch_wide(ctx, src, i1 - i0, w, h, h, 0, dpitch, dstride, k, select,
                                     sub(i0), st);
         }

@@ -132,3 +132,22 @@ def test_fused_rgb_pipelined_and_c3_frame(ctx, orc):
     for o in outs[1:]:
         for key in ("sums", "cards", "t0", "topk"):
             assert torch.equal(o[key], outs[0][key])
+
+
+@pytest.mark.parametrize("w,h,n", [(2048, 2100, 1), (1024, 1500, 3), (64, 48, 1)])
+def test_fused_rgb_host_path(ctx, unfused, orc, w, h, n):
+    """kohler_cuda_analyze_rgb_batch from host memory: uploads in two chunks
+    above 4 Mpx (a row band + its halo row for one image, whole images for a
+    batch), K1 over the uploaded RGB rows."""
+    rng = np.random.default_rng(w + h + n)
+    rgb = np.stack([_image(rng, h, w, "regions") for _ in range(n)])
+    r = ctx.analyze_rgb_batch(rgb, k=6)
+    # one image: [K1 of band 1] + K1 of band 2 + finish; a batch: (K1 + finish) per chunk
+    assert ctx.last_launch_count() == (3 if w * h >= 4 << 20 else 2) if n == 1 else 4
+    r2 = unfused.analyze_rgb_batch(rgb, k=6)
+    for i in range(n):
+        e = orc.analyze(orc.rgb_to_gray(rgb[i]), 6)
+        assert np.array_equal(r.sums[i], e["sum"]) and np.array_equal(r.cards[i], e["card"])
+        assert np.array_equal(r.values[i], e["values"])
+        assert int(r.t0[i]) == e["t0"] and r.thresholds(i) == e["topk"]
+        assert np.array_equal(r2.sums[i], r.sums[i]) and r2.thresholds(i) == r.thresholds(i)
