@@ -208,8 +208,12 @@ def main():
     ap.add_argument("--graph-steps", type=int, default=60,
                     help="N=1: replay the step loop from CUDA graphs of this many consecutive "
                          "steps (PDL edges between them inside the graph); 0 = eager launches")
-    ap.add_argument("--band-depth", type=int, default=1,
+    ap.add_argument("--band-depth", type=int, default=2,
                     help="N>1: pipeline depth of the band kernels (kohler_cuda_set_pipeline_depth)")
+    ap.add_argument("--bucket", type=int, default=8,
+                    help="N>1: steps per all-reduce (the partial curves of this many steps "
+                         "reduced in one NCCL call, their selections in one launch); 1 = one "
+                         "all-reduce per step, overlapped with the next step's band kernel")
     ap.add_argument("--eager-bands", action="store_true",
                     help="N>1 (or --force-bands): launch the band steps eagerly instead of "
                          "replaying them (NCCL all-reduces included) from CUDA graphs")
@@ -281,20 +285,42 @@ def main():
         buf = torch.zeros((copies, max(rows, 1), pitch), dtype=torch.uint8, device=dev)
         if rows:
             buf[:, :rows, :w] = img[ba.lo:ba.hi].to(dev)[None]
-        out = ba.out
+        bucket = max(1, args.bucket)
+        if bucket > 1:
+            ba.enable_buckets(bucket)
+            out = ba.bout
 
-        def step(i):
-            # all-reduce of step i overlapped with step i + 1's band K1; the
-            # selection of step i runs behind it (drain() after the last step)
-            ba.step_pipelined(i, buf[i % copies], pitch)
-        launches_per_step = 2
+            def step(i):
+                # band K1 of step i into slot i % m; every m steps one async
+                # all-reduce of the m partials, then (behind the next bucket's
+                # first band kernel) one selection launch for the previous m
+                ba.step_bucketed(buf[i % copies], pitch)
+            launches_per_step = 2 + 1.0 / bucket  # band K1 + finish per step, a select per bucket
+            parallel = (f"row bands x{world} + 1-row halo; NCCL all-reduce of the 512 u64 partials "
+                        f"of {bucket} steps at once (async, overlapped with the next bucket's band "
+                        "kernels), one selection launch per bucket; strong scaling")
+        else:
+            out = ba.out
+
+            def step(i):
+                # all-reduce of step i overlapped with step i + 1's band K1; the
+                # selection of step i runs behind it (drain() after the last step)
+                ba.step_pipelined(i, buf[i % copies], pitch)
+            launches_per_step = 3  # band K1 + finish, select
+            parallel = (f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64 overlapped "
+                        "with the next step's band kernel, strong scaling")
         bytes_per_step = w * h  # whole job processes the full image per step
-        parallel = (f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64 overlapped with "
-                    "the next step's band kernel, strong scaling")
 
     def drain():
         if bands:
-            ba.drain()
+            if getattr(ba, "m", 0):
+                ba.drain_buckets()
+            else:
+                ba.drain()
+
+    def first_result():
+        tk = out["topk"][0] if out["topk"].dim() == 2 else out["topk"]
+        return int(out["t0"][0]), tk[: int(out["topk_count"][0])].tolist()
 
     # correctness gate before timing (bench.cpp:141-161 semantics)
     step(0)
@@ -305,8 +331,7 @@ def main():
     if rank == 0:
         import oracle
         exp = oracle.Oracle().analyze(img.numpy(), K_TOP)
-        got_t0 = int(out["t0"][0])
-        got_tk = out["topk"][: int(out["topk_count"][0])].tolist()
+        got_t0, got_tk = first_result()
         ok = got_t0 == exp["t0"] and got_tk == exp["topk"]
         if not bands:
             ok = ok and np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"]) \
@@ -346,6 +371,7 @@ def main():
             torch.cuda.synchronize()
             if bands:
                 ba._pending = None
+                ba._bpending, ba._bfill = None, 0
 
     sampler = ClockSampler(dev.index if world == 1 else local).start()
     sampler.wait_first()
@@ -372,8 +398,7 @@ def main():
     clocks = sampler.stop()
     if rank == 0:
         # the replayed / pipelined steps left the last image's full result
-        ok = int(out["t0"][0]) == exp["t0"] and \
-            out["topk"][: int(out["topk_count"][0])].tolist() == exp["topk"]
+        ok = first_result() == (exp["t0"], exp["topk"])
         if not bands:
             ok = ok and np.array_equal(out["sums"].cpu().numpy().view(np.uint64), exp["sum"])
         if not ok:
@@ -453,7 +478,7 @@ def main():
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

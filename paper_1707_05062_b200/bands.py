@@ -89,16 +89,16 @@ class BandedAnalyzer:
             from .api import _raise_for
             _raise_for(rc)
 
-    def _band(self, band, pitch: int, cur: torch.Tensor) -> None:
+    def _band(self, band, pitch: int, cur: torch.Tensor, card_ptr: int = None) -> None:
+        p = cur.data_ptr()
+        pc = p + 2048 if card_ptr is None else card_ptr
         fc = self._fast_calls()
         if fc is None:
-            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1,
-                                       cur.data_ptr(), cur.data_ptr() + 256 * 8)
+            self.ctx.band_curve_device(band, self.w, pitch, self.h, self.r0, self.r1, p, pc)
             return
         lib, h, st, _ = fc
-        p = cur.data_ptr()
         rc = lib.kohler_cuda_band_curve_device(h, band.data_ptr(), self.w, pitch, self.h, self.r0,
-                                               self.r1, p, p + 2048, st)
+                                               self.r1, p, pc, st)
         if rc:
             from .api import _raise_for
             _raise_for(rc)
@@ -130,6 +130,83 @@ class BandedAnalyzer:
             work.wait()  # the compute stream waits for the all-reduce
         self._select(buf)
         self._pending = None
+
+    # ---- bucketed all-reduce -------------------------------------------------
+    # One small all-reduce per step is latency-bound (a few us over NVLink,
+    # longer than a band's K1 at N >= 2).  Bucketed steps put step i's
+    # partial into slot i % m of a [sums m x 256 | cards m x 256] block and
+    # all-reduce the block once per m steps (asynchronously, while the next
+    # bucket accumulates into the other block); the m selections then run
+    # as one select launch.  Every step's result is exact; step i's lands in
+    # ``bout[...][i % m]`` once its bucket is reduced (``drain_buckets()``
+    # completes a partial bucket).
+    def enable_buckets(self, m: int) -> None:
+        dev = self.curve.device
+        k = self.k
+        self.m = int(m)
+        self._blocks = [torch.zeros(2 * self.m * 256, dtype=torch.int64, device=dev)
+                        for _ in range(2)]
+        self.bout = {"values": torch.zeros((self.m, 256), dtype=torch.float64, device=dev),
+                     "defined": torch.zeros((self.m, 256), dtype=torch.uint8, device=dev),
+                     "t0": torch.zeros(self.m, dtype=torch.int32, device=dev),
+                     "topk": torch.zeros((self.m, k), dtype=torch.int32, device=dev),
+                     "topk_count": torch.zeros(self.m, dtype=torch.int32, device=dev),
+                     "status": torch.zeros(self.m, dtype=torch.int32, device=dev)}
+        self._bblock, self._bfill, self._bpending = 0, 0, None
+
+    def step_bucketed(self, band: torch.Tensor, pitch: int) -> None:
+        blk = self._blocks[self._bblock]
+        s = self._bfill
+        if self.r1 > self.r0:
+            self._band(band, pitch, blk[s * 256:(s + 1) * 256],
+                       blk.data_ptr() + (self.m + s) * 256 * 8)
+        else:
+            blk[s * 256:(s + 1) * 256].zero_()
+            blk[(self.m + s) * 256:(self.m + s + 1) * 256].zero_()
+        self._bfill += 1
+        if self._bfill == self.m:
+            self.flush_bucket()
+
+    def flush_bucket(self) -> None:
+        n = self._bfill
+        if n == 0:
+            return
+        blk = self._blocks[self._bblock]
+        work = None
+        if dist.is_available() and dist.is_initialized() and (
+                self.always_reduce or dist.get_world_size(self.group) > 1):
+            work = dist.all_reduce(blk, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.finish_bucket()
+        self._bpending = (work, blk, n)
+        self._bblock ^= 1
+        self._bfill = 0
+
+    def finish_bucket(self) -> None:
+        if self._bpending is None:
+            return
+        work, blk, n = self._bpending
+        if work is not None:
+            work.wait()
+        p = blk.data_ptr()
+        pc = p + self.m * 256 * 8
+        o = self.bout
+        fc = self._fast_calls()
+        if fc is None:
+            self.ctx.select_device(p, pc, n, 256, self.k, o)
+        else:
+            lib, h, st, _ = fc
+            rc = lib.kohler_cuda_select_device(h, p, pc, n, 256, self.k, o["values"].data_ptr(),
+                                               o["defined"].data_ptr(), o["t0"].data_ptr(),
+                                               o["topk"].data_ptr(), o["topk_count"].data_ptr(),
+                                               o["status"].data_ptr(), st)
+            if rc:
+                from .api import _raise_for
+                _raise_for(rc)
+        self._bpending = None
+
+    def drain_buckets(self) -> None:
+        self.flush_bucket()
+        self.finish_bucket()
 
     def step(self, band: torch.Tensor, pitch: int) -> None:
         """band: CUDA uint8 buffer holding rows [lo, hi) with row pitch `pitch`."""

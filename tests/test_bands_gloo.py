@@ -98,16 +98,19 @@ class _OracleCtx:
 
     def select_device(self, sums, cards, n, levels, k, out, stream=None):
         import ctypes
-        s = np.zeros(256, np.uint64)
-        c = np.zeros(256, np.uint64)
-        ctypes.memmove(s.ctypes.data, sums, 2048)
-        ctypes.memmove(c.ctypes.data, cards, 2048)
-        v, d = self.orc.mean_contrast(s, c)
-        st, ts = self.orc.top_k(v, d, k)
-        out["t0"][0] = self.orc.optimal_threshold(v, d)
-        out["topk_count"][0] = len(ts)
-        out["topk"][: len(ts)] = torch.tensor(ts, dtype=torch.int32)
-        out["status"][0] = st
+        for i in range(n):
+            s = np.zeros(256, np.uint64)
+            c = np.zeros(256, np.uint64)
+            ctypes.memmove(s.ctypes.data, sums + 2048 * i, 2048)
+            ctypes.memmove(c.ctypes.data, cards + 2048 * i, 2048)
+            v, d = self.orc.mean_contrast(s, c)
+            st, ts = self.orc.top_k(v, d, k)
+            t0 = out["t0"] if n > 1 or out["t0"].dim() else out["t0"]
+            out["t0"][i] = self.orc.optimal_threshold(v, d)
+            out["topk_count"][i] = len(ts)
+            tk = out["topk"][i] if out["topk"].dim() == 2 else out["topk"]
+            tk[: len(ts)] = torch.tensor(ts, dtype=torch.int32)
+            out["status"][i] = st
 
 
 def _worker_pipelined(rank, world, port, imgs, k, q):
@@ -148,6 +151,69 @@ def test_gloo_pipelined_steps(orc, world):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker_pipelined, args=(r, world, port, imgs, 6, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [(e["t0"], e["topk"]) for e in (orc.analyze(im, 6) for im in imgs)]
+    for _, got in res:
+        assert got == want
+
+
+def _worker_bucketed(rank, world, port, imgs, k, m, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_1707_05062_b200.bands import BandedAnalyzer
+    orc = oracle.Oracle()
+    h, w = imgs[0].shape
+    ctx = _OracleCtx(orc, imgs[0])
+    ba = BandedAnalyzer(ctx, w, h, world, rank, k, device=torch.device("cpu"))
+    ba.enable_buckets(m)
+    got = {}
+
+    def harvest(first, n):
+        for j in range(n):
+            cnt = int(ba.bout["topk_count"][j])
+            got[first + j] = (int(ba.bout["t0"][j]), ba.bout["topk"][j, :cnt].tolist())
+
+    for i, im in enumerate(imgs):
+        ctx.img = im
+        ba.step_bucketed(None, w)
+        if (i + 1) % m == 0 and i + 1 > m:  # the previous bucket was selected
+            harvest(i + 1 - 2 * m, m)
+    full = len(imgs) // m
+    if len(imgs) % m:  # the partial bucket's reduce selects the last full bucket
+        ba.flush_bucket()
+        harvest((full - 1) * m, m)
+        ba.finish_bucket()
+        harvest(full * m, len(imgs) - full * m)
+    else:
+        ba.drain_buckets()
+        harvest((full - 1) * m, m)
+    q.put((rank, [got.get(i) for i in range(len(imgs))]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,n", [(2, 3, 8), (3, 2, 6)])
+def test_gloo_bucketed_steps(orc, world, m, n):
+    """Bucketed all-reduce (one all-reduce of m steps' partials, selection
+    of the m curves in one call): every step's exact thresholds."""
+    rng = np.random.default_rng(200 + world)
+    imgs = []
+    for i in range(n):
+        a = rng.integers(0, 256, (37, 23), dtype=np.uint8)
+        a[3 + i:15 + i] = rng.integers(0, 256)
+        imgs.append(a)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_bucketed, args=(r, world, port, imgs, 6, m, q))
              for r in range(world)]
     for p in procs:
         p.start()
