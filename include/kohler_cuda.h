@@ -196,8 +196,13 @@ int kohler_cuda_rgb_to_gray_device(kohler_cuda_ctx *ctx, const uint8_t *rgb, int
 
 /* The full per-image pipeline of kohler_cuda_analyze_batch on RGB input:
  * fast_contrast_curve(read_pnm(P6 bytes)) + mean_contrast + optimal_threshold
- * + top_k_local_maxima in one call, the grey image existing only in device
- * staging memory.  Host buffers (synchronous) / device buffers (on `stream`). */
+ * + top_k_local_maxima in one call.  When w % 16 == 0 and the rows / images
+ * are 16-byte aligned (device API; the host API stages aligned rows itself)
+ * the accumulation kernel reads the RGB rows and computes the luma itself,
+ * so no grey image is written; otherwise the grey image exists only in device
+ * staging memory.  Results are identical either way (KOHLER_RGB_UNFUSED=1 in
+ * the environment at kohler_cuda_create forces the two-pass form).
+ * Host buffers (synchronous) / device buffers (on `stream`). */
 int kohler_cuda_analyze_rgb_batch(kohler_cuda_ctx *ctx, const uint8_t *rgb, int n, int w, int h,
                                   size_t rgb_pitch, size_t rgb_stride, int k, uint64_t *sums,
                                   uint64_t *cards, double *values, uint8_t *defined, int *t0s,
