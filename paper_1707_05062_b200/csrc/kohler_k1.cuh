@@ -560,7 +560,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     // corr[v] of a pixel with W address A: corr_base + (A >> 6) (A >> 6 = 4v + (lane4 >> 6))
     const uint32_t corr_base = smbase + F::shift + kSmCorr - (lane4 >> 6);
     const int R = p.R;
-    const uint32_t pitch = (uint32_t)p.pitch;  // < 2^31 / 64 (checked by the host)
+    const uint32_t pitch = (uint32_t)p.pitch;  // < 2^32 / (kMaxWalkRows + 32) (checked by the host)
     const bool any = ua < ub;
     // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
     const uint32_t ring = (smbase + kSmRing + 127u) & ~127u;

@@ -38,6 +38,7 @@ using namespace kohler_dev;
 
 namespace {
 
+constexpr int kMaxWalkRows = 128;    // longest K1 column walk (rows)
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
 constexpr int kMaxDepth = 4;         // K1 launches in flight (pipelined mode)
 constexpr int kMaxSelectLevels = 4096;
@@ -53,7 +54,7 @@ struct WideParams {
     int h_total;    // global height
     int r0;         // global row of buffer row 0
     int nseg;       // S: 16-pixel segments per row
-    int R;          // rows per column walk (even)
+    int R;          // rows per column walk (16 .. kMaxWalkRows)
     long long T;    // walk tasks per image (S * ceil(band_rows / R))
     long long gpi;  // 32-lane groups per image
     long long upi;  // units per image: gpi * R (unit = one row of a group's 32 walks)

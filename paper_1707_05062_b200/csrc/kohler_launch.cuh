@@ -127,7 +127,8 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         return KOHLER_OK;
     // rgb: px is interleaved RGB (3 bytes per pixel) and K1 computes the
     // luma itself; the caller guarantees rgb_fused_ok()
-    if (pitch >= (1ull << 31) / 64)
+    // ring positions of a walk address rows by 32-bit (R + 1) * pitch offsets
+    if (pitch >= (1ull << 32) / (kMaxWalkRows + 32))
         return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
     const int nseg = (w + 15) / 16;
     // Pipeline depth d > 1 (finishing launches only): each K1 takes 1/d of
@@ -145,7 +146,9 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     long long R = 64;
     {
         double best = 1e30;
-        for (long long r = 16; r <= 64; ++r) {
+        // up to 128 rows per walk (measured against 64: C2 +1.3 %, C4 +2.6 %,
+        // C3 +0.4 %; the prime positions per walk amortise over more rows)
+        for (long long r = 16; r <= kMaxWalkRows; ++r) {
             const long long ch = (band_rows + r - 1) / r;
             const double waste = (double)(ch * r - band_rows) / band_rows + 0.5 / r;
             if (waste < best - 1e-12) {
