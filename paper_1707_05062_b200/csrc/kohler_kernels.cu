@@ -38,7 +38,10 @@ using namespace kohler_dev;
 
 namespace {
 
-constexpr int kMaxWalkRows = 128;    // longest K1 column walk (rows)
+#ifndef KOHLER_MAX_WALK_ROWS
+#define KOHLER_MAX_WALK_ROWS 128
+#endif
+constexpr int kMaxWalkRows = KOHLER_MAX_WALK_ROWS;  // longest K1 column walk (rows)
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention
 constexpr int kMaxDepth = 4;         // K1 launches in flight (pipelined mode)
 constexpr int kMaxSelectLevels = 4096;
