@@ -30,10 +30,11 @@ INVALID_K = 2
 
 def build(ref: bool = True) -> None:
     """Compile the C restatement and, when /root/reference is present, the
-    reference library (outputs only under oracle/_build and oracle/_ref)."""
+    reference library and the reference's acceptance runner relinked against
+    the drop-in (outputs only under oracle/_build and oracle/_ref)."""
     targets = [ORACLE_SO]
     if ref and os.path.isdir(REFERENCE_SRC):
-        targets.append("ref")
+        targets += ["ref", "acceptance"]
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
