@@ -119,7 +119,13 @@ int kohler_cuda_optimal_threshold(kohler_cuda_ctx *ctx, const double *values,
 int kohler_cuda_top_k_local_maxima(kohler_cuda_ctx *ctx, const double *values,
                                    const uint8_t *defined, int n, int k, int *out, int *count);
 
-/* ---- device-memory API (asynchronous on `stream`, a cudaStream_t) ------ */
+/* ---- device-memory API (asynchronous on `stream`, a cudaStream_t) ------
+ * Output alignment (device pointers): sums / cards / values 16-byte aligned,
+ * defined 8-byte, t0s / topks / topk_counts / status 4-byte (the kernels use
+ * vector accesses; a misaligned pointer is refused with
+ * KOHLER_INVALID_ARGUMENT instead of faulting).  Inputs may have any
+ * alignment and pitch (unaligned ones are staged once); a row pitch must be
+ * below 2^32 bytes. */
 
 /* Batched pipeline on device-resident images (the throughput path).  All
  * pointers are device pointers; outputs as in kohler_cuda_analyze_batch and

@@ -267,22 +267,20 @@ class Context:
         torch.cuda.Stream) or the current torch stream."""
         _raise_for(self._lib.kohler_cuda_analyze_batch_device(
             self._h, _dptr(px), int(n), int(w), int(h), int(pitch), int(image_stride), int(k),
-            _dptr(out.get("sums")), _dptr(out.get("cards")), _dptr(out.get("values")),
-            _dptr(out.get("defined")), _dptr(out.get("t0")), _dptr(out.get("topk")),
-            _dptr(out.get("topk_count")), _dptr(out.get("status")), _stream(stream)))
+            *_outs(out, ("sums", "cards", "values", "defined", "t0", "topk", "topk_count",
+                         "status")), _stream(stream)))
 
     def band_curve_device(self, band, w: int, pitch: int, h_total: int, r0: int, r1: int,
                           sum_, card, stream=None) -> None:
         _raise_for(self._lib.kohler_cuda_band_curve_device(
             self._h, _dptr(band), int(w), int(pitch), int(h_total), int(r0), int(r1),
-            _dptr(sum_), _dptr(card), _stream(stream)))
+            _dptr(sum_, "sums"), _dptr(card, "cards"), _stream(stream)))
 
     def select_device(self, sums, cards, n_curves: int, levels: int, k: int, out: dict,
                       stream=None) -> None:
         _raise_for(self._lib.kohler_cuda_select_device(
-            self._h, _dptr(sums), _dptr(cards), int(n_curves), int(levels), int(k),
-            _dptr(out.get("values")), _dptr(out.get("defined")), _dptr(out.get("t0")),
-            _dptr(out.get("topk")), _dptr(out.get("topk_count")), _dptr(out.get("status")),
+            self._h, _dptr(sums, "sums"), _dptr(cards, "cards"), int(n_curves), int(levels), int(k),
+            *_outs(out, ("values", "defined", "t0", "topk", "topk_count", "status")),
             _stream(stream)))
 
 
@@ -357,9 +355,8 @@ class Context:
                                  n: int, k: int, out: dict, stream=None) -> None:
         _raise_for(self._lib.kohler_cuda_analyze_rgb_batch_device(
             self._h, _dptr(rgb), int(n), int(w), int(h), int(rgb_pitch), int(rgb_stride), int(k),
-            _dptr(out.get("sums")), _dptr(out.get("cards")), _dptr(out.get("values")),
-            _dptr(out.get("defined")), _dptr(out.get("t0")), _dptr(out.get("topk")),
-            _dptr(out.get("topk_count")), _dptr(out.get("status")), _stream(stream)))
+            *_outs(out, ("sums", "cards", "values", "defined", "t0", "topk", "topk_count",
+                         "status")), _stream(stream)))
 
     # ---- segmentation -------------------------------
     def classify(self, px: np.ndarray, thresholds) -> np.ndarray:
@@ -405,8 +402,8 @@ class Context:
                              status, stream=None) -> None:
         _raise_for(self._lib.kohler_cuda_segment_batch_device(
             self._h, _dptr(px), int(n), int(w), int(h), int(pitch), int(image_stride), int(k),
-            _dptr(out), int(out_pitch), int(out_stride), _dptr(thresholds), _dptr(counts),
-            _dptr(status), _stream(stream)))
+            _dptr(out), int(out_pitch), int(out_stride), _dptr(thresholds, "topk"),
+            _dptr(counts, "topk_count"), _dptr(status, "status"), _stream(stream)))
 
 
 def _alloc_result(n: int, k: int, curves: bool, mean: bool) -> BatchResult:
@@ -423,12 +420,37 @@ def _optr(a):
     return None if a is None else a.ctypes.data
 
 
-def _dptr(t):
+_OUT_DTYPES = {"sums": ("int64", "uint64"), "cards": ("int64", "uint64"), "values": ("float64",),
+               "defined": ("uint8", "bool"), "t0": ("int32",), "topk": ("int32",),
+               "topk_count": ("int32",), "status": ("int32",)}
+
+
+def _dptr(t, kind: str = None):
+    """Device pointer of a CUDA tensor (or a raw int pointer, passed through).
+    ``kind``: None for an image buffer (uint8, any strides: the pitch is
+    explicit), else an output name of _OUT_DTYPES (contiguous, that dtype).
+    A CPU tensor or a wrong dtype would silently compute garbage or fault in
+    the kernel, so it is refused here."""
     if t is None:
         return None
     if isinstance(t, int):
         return t
+    if not getattr(t, "is_cuda", False):
+        raise ValueError("device API: expected a CUDA tensor")
+    dt = str(t.dtype).replace("torch.", "")
+    if kind is None:
+        if dt != "uint8":
+            raise ValueError(f"device API: image buffers must be uint8, got {dt}")
+    else:
+        if dt not in _OUT_DTYPES[kind]:
+            raise ValueError(f"device API: '{kind}' must be {' or '.join(_OUT_DTYPES[kind])}, got {dt}")
+        if not t.is_contiguous():
+            raise ValueError(f"device API: '{kind}' must be contiguous")
     return t.data_ptr()
+
+
+def _outs(out: dict, names) -> list:
+    return [_dptr(out.get(n), n) for n in names]
 
 
 def _stream(s):

@@ -1,218 +1,15 @@
-// kohler_device.cuh — device building blocks of the sm_100a Köhler path.
-//
-// Accumulation ("K1").  Every unordered 4-neighbour pair (a,b)
-// with lo = min, hi = max, s = a + b is reduced to O(1) integer updates:
-//     H_hi[hi] += 1, H_s[s] += 1            (per pair; equal pairs included)
-//     hist[a]  += 1                          (per pixel, as the 'cur' row)
-// The curve is rebuilt exactly from these:
-//     P      = 4*hist - corr                 (degree-weighted pixel histogram)
-//     card[t]= sum_{v<=t} (P[v] - 2 H_hi[v])
-//     sum[t] = sum_{u<=t} sum_{u'<=u} ( P[u'-1] - H_s[2u'-3] - 2 H_s[2u'-2] - H_s[2u'-1] )
-// because the tent min(hi-t, t-lo) on [lo,hi) (proj/src/kernels/pair_tent.hpp:12-18)
-// has second difference +1 at lo+1 and hi+1 and -1 at floor(s/2)+1 and
-// ceil(s/2)+1, and equal pairs cancel exactly.  `corr` holds the border
-// terms (missing neighbours) and the compensation for the equal "fake" pairs
-// the universal lane path creates at row ends (see border_terms()).
-//
-// Histogram layout in shared memory (128 KiB, "lane-striped"): 512 rows of
-// 256 bytes; word (row, half, lane) lives at row*256 + half*128 + lane*4, so
-// lane L only ever touches bank L and every warp-wide update is
-// bank-conflict free whatever the keys are.  half 0 of row r holds H_s[r]
-// (r = 0..510), half 1 of rows 0..255 holds hist[v], half 1 of rows
-// 256..511 holds H_hi[v].  The byte address (key << 8) | lane*4 is one PRMT.
+// kohler_device.cuh — device helpers shared by the sm_100a kernels:
+// the int64 prefix scans that rebuild a curve from its 512 combinations
+// (card first differences, sum second differences; DESIGN.md §2 and the
+// derivation in kohler_walk.cuh) and the K4 selection (mean contrast,
+// optimal threshold, top-k local maxima; proj/src/threshold.cpp:9-82)
+// used by finish_kernel, K5's flush and the select kernels.  The
+// accumulation itself lives in kohler_walk.cuh / kohler_k1.cuh / kohler_k5.cuh.
 #pragma once
 
 #include <cstdint>
 
 namespace kohler_dev {
-
-constexpr int kLevels = 256;
-constexpr uint32_t kStripedBytes = 512u * 256u;
-constexpr uint32_t kOffHs = 0;             // + (s << 8) | lane4
-constexpr uint32_t kOffHist = 128;         // + (v << 8) | lane4
-constexpr uint32_t kOffHhi = 65536 + 128;  // + (v << 8) | lane4
-
-__device__ __forceinline__ void inc(unsigned char* base, uint32_t off)
-{
-    atomicAdd(reinterpret_cast<uint32_t*>(base + off), 1u);
-}
-
-// Four pairs packed in 16-bit lanes: x = [a0, a2], y = [b0, b2] (one byte per
-// 16-bit lane, upper byte zero).  Two pairs per call.
-__device__ __forceinline__ void pairs2(unsigned char* sm, uint32_t x, uint32_t y, uint32_t lane4)
-{
-    const uint32_t hx = __vmaxu2(x, y);  // VIMNMX.U16x2
-    const uint32_t sx = x + y;           // no carry between halves (<= 510)
-    inc(sm + kOffHhi, __byte_perm(hx, lane4, 0x5504));
-    inc(sm + kOffHhi, __byte_perm(hx, lane4, 0x5524));
-    inc(sm + kOffHs, __byte_perm(sx, lane4, 0x5104));
-    inc(sm + kOffHs, __byte_perm(sx, lane4, 0x5324));
-}
-
-__device__ __forceinline__ void pixels4(unsigned char* sm, uint32_t c, uint32_t lane4)
-{
-    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5504));
-    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5514));
-    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5524));
-    inc(sm + kOffHist, __byte_perm(c, lane4, 0x5534));
-}
-
-// All updates of one 16-pixel segment: 16 right pairs (the 16th against rn),
-// 16 down pairs (cur vs nxt) and 16 pixels.  80 conflict-free ATOMS.
-__device__ __forceinline__ void accumulate_segment(unsigned char* sm, const uint32_t (&c)[4],
-                                                   const uint32_t (&n)[4], uint32_t rn,
-                                                   uint32_t lane4)
-{
-    uint32_t ce[5];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        ce[j] = __byte_perm(c[j], 0, 0x4240);  // [b0, b2]
-    ce[4] = rn & 0xFFu;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint32_t co = __byte_perm(c[j], 0, 0x4341);          // [b1, b3]
-        const uint32_t ro = __byte_perm(ce[j], ce[j + 1], 0x1412); // [b2, next b0]
-        const uint32_t ne = __byte_perm(n[j], 0, 0x4240);
-        const uint32_t no = __byte_perm(n[j], 0, 0x4341);
-        pairs2(sm, ce[j], co, lane4);  // right pairs (b0,b1), (b2,b3)
-        pairs2(sm, co, ro, lane4);     // right pairs (b1,b2), (b3,next)
-        pairs2(sm, ce[j], ne, lane4);  // down pairs, columns 0 and 2
-        pairs2(sm, co, no, lane4);     // down pairs, columns 1 and 3
-        pixels4(sm, c[j], lane4);
-    }
-}
-
-// Byte i (compile-time index after unrolling) of a 16-byte segment.
-__device__ __forceinline__ uint32_t byte_at(const uint32_t (&c)[4], int i)
-{
-    return (c[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-}
-
-// Byte e (runtime index, 0..15) without dynamic register indexing (which
-// would force the segment into local memory).
-__device__ __forceinline__ uint32_t byte_dyn(const uint32_t (&c)[4], int e)
-{
-    const uint32_t wd = e < 4 ? c[0] : e < 8 ? c[1] : e < 12 ? c[2] : c[3];
-    return (wd >> (8 * (e & 3))) & 0xFFu;
-}
-
-// Replace bytes i > e of the segment by v (row-end lanes).
-__device__ __forceinline__ void fill_tail(uint32_t (&c)[4], int e, uint32_t v)
-{
-    const uint32_t vvvv = v * 0x01010101u;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int keep = e - 4 * j + 1;  // bytes of word j to keep
-        if (keep <= 0)
-            c[j] = vvvv;
-        else if (keep < 4) {
-            const uint32_t m = 0xFFFFFFFFu << (8 * keep);
-            c[j] = (c[j] & ~m) | (vvvv & m);
-        }
-    }
-}
-
-template <bool VEC>
-__device__ __forceinline__ void load_segment(const uint8_t* row, int x0, int w, uint32_t (&c)[4])
-{
-    if (VEC) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + x0));
-        c[0] = v.x;
-        c[1] = v.y;
-        c[2] = v.z;
-        c[3] = v.w;
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int x = x0 + 4 * j + b;
-                const uint32_t byte = x < w ? __ldg(row + x) : 0u;
-                word |= byte << (8 * b);
-            }
-            c[j] = word;
-        }
-    }
-}
-
-// Geometry of one 16-pixel segment step, band-relative.
-struct StepGeom {
-    int w;         // image width
-    int y;         // band-relative row of `cur`
-    int band_rows; // own rows of the band
-    int gy;        // global row of `cur`
-    int h_total;   // global image height
-    int x0;        // first column of the segment
-};
-
-// One lane's step: fix up row ends / last rows so that every lane runs the
-// same predicate-free accumulate_segment, and record the border terms.
-//
-// Row-end lane (x0 + 16 >= w, e = w-1-x0): bytes > e of cur and nxt and the
-// right neighbour are replaced by v = cur[e].  The resulting equal "fake"
-// pairs cancel in the reconstruction once P counts them: the garbage pixels'
-// 4*hist supplies 4(15-e), the fake pairs need 2(16-e) + 2(15-e), so corr[v]
-// gets -2, plus +1 for pixel e's missing right pair: -1 in total.
-// Last image row: nxt := cur, so every down pair is an equal fake pair:
-// corr += 1 (missing down pair) - 2 (fake) = -1 per real pixel.
-// Band-first row: +1 per real pixel (its up pair belongs to the row above /
-// does not exist).  Row start: +1 (no left pair).  Halo row pixels (row r1 of
-// a band with r1 < h): -1 each (their up pair is owned, P gains 1).
-// `corr` is lane-striped like the histograms (word (v, lane) at
-// v*128 + lane*4, 32 KiB) so its updates are bank-conflict free, and the
-// per-pixel loops are branch-free (a disabled term adds 0).
-__device__ __forceinline__ void corr_add(unsigned char* corr, uint32_t lane4, uint32_t v, int d)
-{
-    atomicAdd(reinterpret_cast<int*>(corr + (v << 7) + lane4), d);
-}
-
-struct StripedCorr {  // K1: lane-striped corr (conflict free)
-    unsigned char* base;
-    uint32_t lane4;
-    __device__ __forceinline__ void operator()(uint32_t v, int d) const { corr_add(base, lane4, v, d); }
-};
-
-struct PlainCorr {  // K5: one 256-entry corr array per image group
-    int* base;
-    __device__ __forceinline__ void operator()(uint32_t v, int d) const { atomicAdd(base + v, d); }
-};
-
-template <class CorrAdd>
-__device__ __forceinline__ void border_terms(const CorrAdd& corr, const StepGeom& g,
-                                             uint32_t (&c)[4], uint32_t (&n)[4], uint32_t& rn,
-                                             bool has_down)
-{
-    const int e = g.w - 1 - g.x0;  // index of the last real pixel if < 16
-    if (g.x0 == 0)
-        corr(c[0] & 0xFFu, 1);
-    // +1 (band-first row: no owned up pair), -1 (last image row: missing down
-    // pair +1, fake equal down pair -2); both at once cancel.
-    const int dcur = (g.y == 0 ? 1 : 0) - (has_down ? 0 : 1);
-    if (dcur != 0) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            corr(byte_at(c, i), i <= e ? dcur : 0);
-    }
-    if (has_down && g.y + 1 == g.band_rows) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            corr(byte_at(n, i), i <= e ? -1 : 0);
-    }
-    if (e <= 15) {
-        const uint32_t v = byte_dyn(c, e);
-        fill_tail(c, e, v);
-        if (has_down)
-            fill_tail(n, e, v);
-        rn = v;
-        corr(v, -1);
-    }
-    if (!has_down) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            n[j] = c[j];
-    }
-}
 
 // ---- exact reconstruction ------------------------------------------------
 
@@ -242,55 +39,8 @@ __device__ __forceinline__ void warp_prefix256(const long long* in, long long* o
 
 // Count and sum of one curve from its 512 combinations, by one warp, lane
 // owning thresholds [8*lane, 8*lane+8): card = prefix(cd), sum =
-// prefix(prefix(h2)).  cd(t)/h2(u) are functors; results go to card[]/sum[].
-template <class CD, class H2>
-__device__ __forceinline__ void warp_curve256(CD cd, H2 h2, uint64_t* card, uint64_t* sum)
-{
-    const int lane = threadIdx.x & 31;
-    long long a[8], g[8];
-    long long ra = 0, rg = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        ra += cd(lane * 8 + j);
-        a[j] = ra;
-        rg += h2(lane * 8 + j);
-        g[j] = rg;
-    }
-    long long xa = ra, xg = rg;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const long long ya = __shfl_up_sync(0xFFFFFFFFu, xa, off);
-        const long long yg = __shfl_up_sync(0xFFFFFFFFu, xg, off);
-        if (lane >= off) {
-            xa += ya;
-            xg += yg;
-        }
-    }
-    const long long ea = xa - ra, eg = xg - rg;
-    long long rs = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        a[j] += ea;
-        g[j] += eg;
-        rs += g[j];
-        g[j] = rs;
-    }
-    long long xs = rs;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const long long ys = __shfl_up_sync(0xFFFFFFFFu, xs, off);
-        if (lane >= off)
-            xs += ys;
-    }
-    const long long es = xs - rs;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        card[lane * 8 + j] = (uint64_t)a[j];
-        sum[lane * 8 + j] = (uint64_t)(g[j] + es);
-    }
-}
-
-// Same as warp_curve256 but returns each lane's 8 (card, sum) in registers.
+// prefix(prefix(h2)); cd(t) / h2(u) are functors.  Each lane's 8 (card, sum)
+// are returned in registers.
 template <class CD, class H2>
 __device__ __forceinline__ void warp_curve256_regs(CD cd, H2 h2, uint64_t (&card)[8],
                                                    uint64_t (&sum)[8])
@@ -334,26 +84,6 @@ __device__ __forceinline__ void warp_curve256_regs(CD cd, H2 h2, uint64_t (&card
 #pragma unroll
     for (int j = 0; j < 8; ++j)
         sum[j] = (uint64_t)(g[j] + es);
-}
-
-// The 512 linear combinations one partial contributes: cd[v] (count first
-// difference) in [0,256) and h2[u] (sum second difference) in [256,512).
-// hist(v), hhi(v), hs(s) read the partial's reduced histograms.
-template <class Hist, class Hhi, class Hs, class Corr>
-__device__ __forceinline__ long long combo(int t, Hist hist, Hhi hhi, Hs hs, Corr corr)
-{
-    if (t < 256) {
-        const long long p = 4ll * (long long)hist(t) - (long long)corr(t);
-        return p - 2ll * (long long)hhi(t);
-    }
-    const int u = t - 256;
-    if (u == 0)
-        return 0;
-    const long long p = 4ll * (long long)hist(u - 1) - (long long)corr(u - 1);
-    long long r = p - 2ll * (long long)hs(2 * u - 2) - (long long)hs(2 * u - 1);
-    if (u >= 2)
-        r -= (long long)hs(2 * u - 3);
-    return r;
 }
 
 // ---- selection (K4): mean contrast, optimal threshold, top-k maxima ------

@@ -16,6 +16,7 @@
 // One process-wide context on device $KOHLER_CUDA_DEVICE (default 0) is
 // created on first use; calls are serialised on it, so concurrent callers are
 // safe and get identical results.  No CPU fallback: failures throw.
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -157,6 +158,8 @@ ThresholdSet top_k_local_maxima(const MeanContrastCurve& mc, int k)
     const FlatMean f(mc);
     if (f.values.empty())
         throw NoBoundaryError{};
+    // at most levels maxima exist: a huge k means "all of them", cheaply
+    k = static_cast<int>(std::min<std::size_t>(static_cast<std::size_t>(k), f.values.size()));
     std::vector<int> out(static_cast<std::size_t>(k));
     int count = 0;
     raise_for(kohler_cuda_top_k_local_maxima(context(), f.values.data(), f.defined.data(),

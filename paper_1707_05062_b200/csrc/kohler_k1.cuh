@@ -357,8 +357,8 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
 template <bool RGB>
 __device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitch, uint32_t dst)
 {
-    const uint32_t off = (uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
-    const uint8_t* src = L.p + off;
+    // 64-bit row offset (once per segment start: no cost in the walk)
+    const uint8_t* src = L.p + (size_t)(uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
     if constexpr (RGB) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
@@ -397,7 +397,7 @@ __device__ __forceinline__ FetchStream fetch_stream(const LaneGeo& L, int j, uin
 {
     FetchStream f;
     const int jj = min(j, L.jcl);  // j >= 3 > jlo
-    f.src = L.p + (size_t)((uint32_t)jj * pitch);
+    f.src = L.p + (size_t)(uint32_t)jj * pitch;
     f.left = L.jcl - j;
     f.pl = L.pad && lane == 0;
     f.pr = L.pad && lane == 31;
@@ -560,7 +560,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     // corr[v] of a pixel with W address A: corr_base + (A >> 6) (A >> 6 = 4v + (lane4 >> 6))
     const uint32_t corr_base = smbase + F::shift + kSmCorr - (lane4 >> 6);
     const int R = p.R;
-    const uint32_t pitch = (uint32_t)p.pitch;  // < 2^32 / (kMaxWalkRows + 32) (checked by the host)
+    const uint32_t pitch = (uint32_t)p.pitch;  // < 2^32 (checked by the host)
     const bool any = ua < ub;
     // this lane's segment in slot 0 of the warp's ring; slot s is + s * kSlotBytes
     const uint32_t ring = (smbase + kSmRing + 127u) & ~127u;
@@ -633,9 +633,11 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 asm volatile("cp.async.wait_group 2;" ::: "memory");
             else
                 asm volatile("cp.async.wait_group 1;" ::: "memory");
+#ifndef KOHLER_NO_RING_SYNCWARP
             // all lanes' copies into slot q & 3 are visible, and all lanes have
             // read slot (q - 1) & 3 (the previous position), which is refilled now
             __syncwarp();
+#endif
             // read this position's row first: the prefetch issue below
             // covers the LDS latency before the unpack needs the data
             Row r;

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                                      hs[2 * i + 2];
             }
             // hs[0] (row 2 t0 - 3) is counted for u = t0 only when u >= 2: a
-            // negative row is 0 already, so the formula matches warp_curve256's
+            // negative row is 0 already, so the formula matches warp_curve256_regs'
             uint32_t hist_keep[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             TWCYC(1);
             // 2. per-image totals into a padded scratch carved out of the (now
             //    zero) counter block: hs[s] at s + s/16, the other arrays at
-            //    x + x/8 (conflict-free lane-blocked reads of warp_curve256)
+            //    x + x/8 (conflict-free lane-blocked reads of warp_curve256_regs)
             uint32_t* scr = reinterpret_cast<uint32_t*>(hist);
 #pragma unroll
             for (int q = 0; q < PER; ++q) {

@@ -545,6 +545,9 @@ int kohler_cuda_analyze_batch_device(kohler_cuda_ctx* ctx, const uint8_t* px, in
         return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
     if (n > 1 && image_stride < pitch * (size_t)h)
         return fail(KOHLER_INVALID_ARGUMENT, "image stride smaller than one image");
+    rc = check_out_align(sums, cards, values, defined, t0s, topks, topk_counts, status);
+    if (rc)
+        return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     ctx->last_launches = 0;
@@ -742,6 +745,9 @@ int kohler_cuda_analyze_rgb_batch_device(kohler_cuda_ctx* ctx, const uint8_t* rg
         return rc;
     if (k < 1)
         return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    rc = check_out_align(sums, cards, values, defined, t0s, topks, topk_counts, status);
+    if (rc)
+        return rc;
     if (n == 0)
         return KOHLER_OK;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -873,6 +879,8 @@ int kohler_cuda_band_curve_device(kohler_cuda_ctx* ctx, const uint8_t* band, int
         return rc;
     if (r0 < 0 || r1 <= r0 || r1 > h_total)
         return fail(KOHLER_INVALID_ARGUMENT, "band rows must satisfy 0 <= r0 < r1 <= h");
+    if (reinterpret_cast<uintptr_t>(sum) % 8 || reinterpret_cast<uintptr_t>(card) % 8)
+        return fail(KOHLER_INVALID_ARGUMENT, "device sum / card must be 8-byte aligned");
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     ctx->last_launches = 0;
@@ -891,6 +899,8 @@ int kohler_cuda_select_device(kohler_cuda_ctx* ctx, const uint64_t* sums, const 
         return fail(KOHLER_INVALID_ARGUMENT, "levels must be in [1, 4096]");
     if (k < 1)
         return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
+    if (int rc = check_out_align(sums, cards, values, defined, t0s, topks, topk_counts, status))
+        return rc;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     ctx->last_launches = 0;
@@ -1013,6 +1023,9 @@ int kohler_cuda_top_k_local_maxima(kohler_cuda_ctx* ctx, const double* values,
         return fail(KOHLER_INVALID_ARGUMENT, "top_k_local_maxima: k must be at least 1");
     if (!out)
         return fail(KOHLER_INVALID_ARGUMENT, "NULL argument");
+    // at most n maxima exist: a larger k means "all of them" (the reference
+    // truncates a shorter list); clamping keeps the staging O(n)
+    k = std::min(k, std::max(n, 1));
     int st = 0, t0 = -1;
     const int rc =
         host_select(ctx, nullptr, nullptr, values, defined, n, k, nullptr, nullptr, &t0, out, count, &st);

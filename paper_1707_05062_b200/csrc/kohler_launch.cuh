@@ -81,7 +81,26 @@ bool rgb_fused_ok(const kohler_cuda_ctx* ctx, const uint8_t* rgb, int n, int w, 
                   size_t stride)
 {
     return ctx->rgb_fused && w % 16 == 0 && reinterpret_cast<uintptr_t>(rgb) % 16 == 0 &&
-           pitch % 16 == 0 && (n == 1 || stride % 16 == 0) && !use_tile(n, w, h);
+           pitch % 16 == 0 && pitch < (1ull << 32) && (n == 1 || stride % 16 == 0) &&
+           !use_tile(n, w, h);
+}
+
+// Device output arrays are written (and the curves of the selection kernels
+// read) with vector accesses: sums / cards / values 16-byte, defined 8-byte,
+// the int arrays 4-byte aligned.  A misaligned pointer would raise a sticky
+// cudaErrorMisalignedAddress, so it is refused up front.
+int check_out_align(const void* sums, const void* cards, const void* values, const void* defined,
+                    const void* t0s, const void* topks, const void* counts, const void* status)
+{
+    auto mis = [](const void* p, uintptr_t a) { return p && reinterpret_cast<uintptr_t>(p) % a; };
+    if (mis(sums, 16) || mis(cards, 16) || mis(values, 16))
+        return fail(KOHLER_INVALID_ARGUMENT,
+                    "device sums / cards / values must be 16-byte aligned");
+    if (mis(defined, 8))
+        return fail(KOHLER_INVALID_ARGUMENT, "device defined array must be 8-byte aligned");
+    if (mis(t0s, 4) || mis(topks, 4) || mis(counts, 4) || mis(status, 4))
+        return fail(KOHLER_INVALID_ARGUMENT, "device int outputs must be 4-byte aligned");
+    return KOHLER_OK;
 }
 
 int check_image(int n, int w, int h, size_t pitch)
@@ -127,9 +146,10 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         return KOHLER_OK;
     // rgb: px is interleaved RGB (3 bytes per pixel) and K1 computes the
     // luma itself; the caller guarantees rgb_fused_ok()
-    // ring positions of a walk address rows by 32-bit (R + 1) * pitch offsets
-    if (pitch >= (1ull << 32) / (kMaxWalkRows + 32))
-        return fail(KOHLER_INVALID_ARGUMENT, "row pitch too large");
+    // the walk advances its row pointers by a 32-bit pitch (row offsets
+    // themselves are 64-bit): any row below 4 GiB
+    if (pitch >= (1ull << 32))
+        return fail(KOHLER_INVALID_ARGUMENT, "row pitch must be below 2^32 bytes");
     const int nseg = (w + 15) / 16;
     // Pipeline depth d > 1 (finishing launches only): each K1 takes 1/d of
     // the SMs (one more per launch for its finish_kernel) and triggers its
@@ -575,12 +595,16 @@ int host_batch(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, siz
     for (int c = 0; c < chunks; ++c) {
         if (n == 1) {
             const int a = bound[c], e = bound[c + 1];
-            rc = upload(0, 1, a, std::min(e + 1, h));  // + the band's halo row
+            // + the band's halo row; a later chunk starts one row down (its
+            // first row is the previous chunk's halo, which that chunk's
+            // kernels may still be reading: never rewrite it)
+            const int a_up = c ? a + 1 : a;
+            rc = a_up < std::min(e + 1, h) ? upload(0, 1, a_up, std::min(e + 1, h)) : KOHLER_OK;
             if (rc)
                 return rc;
             KC_CUDA(cudaEventRecord(ctx->chunk_ev[c], cs));
             KC_CUDA(cudaStreamWaitEvent(st, ctx->chunk_ev[c], 0));
-            rc = to_gray(0, 1, a, std::min(e + 1, h));
+            rc = a_up < std::min(e + 1, h) ? to_gray(0, 1, a_up, std::min(e + 1, h)) : KOHLER_OK;
             if (rc)
                 return rc;
             rc = fused ? launch_wide(ctx, dup + (size_t)a * upitch, 1, w, e - a, h, a, upitch, ustride,
