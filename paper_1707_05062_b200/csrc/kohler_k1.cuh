@@ -70,10 +70,10 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishParams p)
         const double v = cc ? (double)cs / (double)cc : 0.0;
         mean[tid] = v;
         def[tid] = cc ? 1 : 0;
-        if (p.sums) {
+        if (p.sums)
             p.sums[(size_t)img * 256 + tid] = cs;
+        if (p.cards)
             p.cards[(size_t)img * 256 + tid] = cc;
-        }
         if (p.values)
             p.values[(size_t)img * 256 + tid] = v;
         if (p.defined)

@@ -415,12 +415,17 @@ int launch_tile(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int h, si
     tp.sums = o.sums;
     tp.cards = o.cards;
     tp.hist_out = hist_out;
-    if (!tp.sums) {
+    if (!tp.sums || !tp.cards) {
+        // K5 writes both curves (the selection reads them): a missing one
+        // goes to the workspace
         int rc = ctx->curves.ensure((size_t)n * 512 * sizeof(uint64_t));
         if (rc)
             return rc;
-        tp.sums = static_cast<uint64_t*>(ctx->curves.p);
-        tp.cards = tp.sums + (size_t)n * 256;
+        uint64_t* ws = static_cast<uint64_t*>(ctx->curves.p);
+        if (!tp.sums)
+            tp.sums = ws;
+        if (!tp.cards)
+            tp.cards = ws + (size_t)n * 256;
     }
     const bool vec = (reinterpret_cast<uintptr_t>(px) % 16 == 0) && (pitch % 16 == 0) &&
                      (image_stride % 16 == 0);

@@ -74,3 +74,33 @@ def test_rows_wider_than_old_pitch_limit(ctx, orc):
     assert np.array_equal(out["sums"][0].cpu().numpy().view(np.uint64), e["sum"])
     assert np.array_equal(out["cards"][0].cpu().numpy().view(np.uint64), e["card"])
     assert int(out["t0"][0]) == e["t0"]
+
+
+@pytest.mark.parametrize("shape", [(1, 300, 260), (40, 128, 128)])  # K1 and K5 paths
+def test_partial_output_sets(ctx, orc, shape):
+    """Any output pointer may be NULL (include/kohler_cuda.h): sums without
+    cards, cards without sums, thresholds only."""
+    g = torch.Generator(device="cpu")
+    g.manual_seed(11)
+    x = torch.randint(0, 256, shape, generator=g, dtype=torch.uint8)
+    n, h, w = shape
+    exp = [orc.analyze(x[i].numpy(), 6) for i in range(n)]
+    xd = x.cuda()
+    for keys in (("sums",), ("cards",), ("t0", "topk_count"), ("sums", "t0")):
+        out = {}
+        for k in keys:
+            if k in ("sums", "cards"):
+                out[k] = torch.zeros((n, 256), dtype=torch.int64, device="cuda")
+            else:
+                out[k] = torch.zeros(n, dtype=torch.int32, device="cuda")
+        if "topk_count" in out:
+            out["topk"] = torch.zeros((n, 6), dtype=torch.int32, device="cuda")
+        ctx.analyze_batch_device(xd, w, h, w, w * h, n, 6, out)
+        torch.cuda.synchronize()
+        for i in range(n):
+            if "sums" in out:
+                assert np.array_equal(out["sums"][i].cpu().numpy().view(np.uint64), exp[i]["sum"])
+            if "cards" in out:
+                assert np.array_equal(out["cards"][i].cpu().numpy().view(np.uint64), exp[i]["card"])
+            if "t0" in out:
+                assert int(out["t0"][i]) == exp[i]["t0"]

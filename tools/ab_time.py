@@ -29,6 +29,7 @@ for name in a.configs.split(","):
     copies = max(1, int(2 * l2 // x.numel()) + 1) if x.numel() < 2 * l2 else 1
     bufs = torch.stack([x] * copies) if copies > 1 else x[None]
     o = {"sums": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
+         "cards": torch.zeros((n, 256), dtype=torch.int64, device="cuda"),
          "t0": torch.zeros(n, dtype=torch.int32, device="cuda"),
          "topk": torch.zeros((n, 6), dtype=torch.int32, device="cuda"),
          "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda")}
@@ -36,6 +37,8 @@ for name in a.configs.split(","):
 
     def step(i):
         ctx.analyze_batch_device(bufs[i % copies], w, h, w, w * h, n, 6, o)
+    step(0)  # workspace allocations happen outside the capture
+    torch.cuda.synchronize()
     g = bench.GraphSteps(step, 5, STEPS[name])
     best = 0.0
     for _ in range(a.reps):
