@@ -38,16 +38,28 @@ __device__ __forceinline__ int pad8(int x) { return x + (x >> 3); }    // 9*lane
 __device__ __forceinline__ int pad16(int x) { return x + (x >> 4); }   // 17*lane + c
 constexpr int kTwImgWords = (kTwH + 4 * kTwArr + 3) / 4 * 4;
 
+// Per-group border-term arrays int[256] at a 1040-byte stride: the 8 groups'
+// arrays start in different 16-byte bank quads, so the flush's per-group
+// LDS.128 reads of a quarter warp are conflict free (a 1024-byte stride made
+// them 8-way conflicts, ncu r7).
+constexpr uint32_t kTwCorrStride = 1040;
+
 template <int LG>
 struct TwLayout {
     static constexpr int NG = 32 / LG;
+    // LG = 4 (8 images per round, walks of <= 31 rows): one W copy (a lane
+    // word takes <= 16 warps * 31 rows * 16 px <= 8191 events per round)
+    static constexpr bool kOneW = LG == 4;
     // 32 lane segments (512 B, 128-byte aligned), then 2 pads per group
     static constexpr uint32_t kSlot = (512 + 32 * NG + 127) / 128 * 128;
     static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
     static constexpr uint32_t kRingBytes = kTwWarps * kRingSlots * kSlot + 128;
-    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][256]
-    static constexpr uint32_t kTot = kCorr + NG * 1024;  // i64 [3][16 warps][NG] scan carries
-    static constexpr uint32_t kEnd = kTot + 3 * 16 * NG * 8;
+    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][260]
+    static constexpr uint32_t kTot = kCorr + NG * kTwCorrStride;  // i64 [3][16 warps][NG] scan carries
+    // LG = 4 flush: boundary values handed from warp w - 1 to warp w
+    static constexpr uint32_t kXch = kTot + 3 * 16 * NG * 8;  // uint4 [16 warps][8 images]
+    static constexpr uint32_t kXchC = kXch + 16 * 8 * 16;     // int [16 warps][8 images]
+    static constexpr uint32_t kEnd = kXchC + 16 * 8 * 4;
     static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
 };
 
@@ -92,8 +104,17 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
     const uint32_t lane4 = (uint32_t)lane * 4u;
     const uint32_t kneg = kHistAbs - lane4;
     const uint32_t dummy = kHistAbs + kDummy + lane4;
-    const uint32_t corr_g = smbase + Lay::kCorr + (uint32_t)g * 1024u;
+    const uint32_t corr_g = smbase + Lay::kCorr + (uint32_t)g * kTwCorrStride;
     const uint32_t corr_base = corr_g - (lane4 >> 6);
+    // border term corr[v] += d of a pixel with W address A: with one W copy
+    // (LG = 4) the unused second copy is a lane-striped corr table (conflict
+    // free, no address arithmetic); otherwise the per-group int arrays
+    auto corr_add = [&](uint32_t A, uint32_t d) {
+        if constexpr (Lay::kOneW)
+            red_add_imm<kHistAbs + kOffW1>(A, d);
+        else
+            red_add(corr_base + (A >> 6), d);
+    };
     const uint32_t pitch = (uint32_t)p.pitch;
     const int task = warp * LG + lig;
     const int P = p.R + 2;
@@ -118,7 +139,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         uint4* z = reinterpret_cast<uint4*>(hist);
         for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
             z[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < NG * 256; i += kTwThreads)
+        for (int i = tid; i < NG * (int)(kTwCorrStride / 4); i += kTwThreads)
             reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
     }
     __syncthreads();
@@ -147,7 +168,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             constexpr int KIND = decltype(kind)::value;
             constexpr int WC = decltype(wc)::value;
             constexpr bool CROSS = decltype(cross)::value;
-            constexpr uint32_t kOffW = WC ? kOffW1 : kOffW0;
+            constexpr uint32_t kOffW = (WC && !Lay::kOneW) ? kOffW1 : kOffW0;
             const uint32_t q = pos + (uint32_t)j;
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             __syncwarp();
@@ -167,6 +188,14 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 for (int jj = 0; jj < 4; ++jj) {
                     D.ue[jj] = has_up ? qstep(qfrom(C.e[jj]), D.e[jj]) : kNeutral;
                     D.uo[jj] = has_up ? qstep(qfrom(C.o[jj]), D.o[jj]) : kNeutral;
+                }
+                // the image's first row (no up pairs): corr +1 per pixel, from
+                // the row just absorbed (no global re-read after the walk)
+                if (G.nrows > 0 && !has_up) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (ALIGNED || i <= G.e)
+                            corr_add(D.A[i], 1u);
                 }
             }
             if (KIND < 2)
@@ -204,9 +233,9 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             }
             if (F.edge && live) {
                 if (row_start)
-                    red_add(corr_base + (C.A[0] >> 6), 1u);
+                    corr_add(C.A[0], 1u);
                 if (row_end)
-                    red_add(corr_base + (Arn >> 6), 0xFFFFFFFFu);
+                    corr_add(Arn, 0xFFFFFFFFu);
             }
         };
         using K0 = std::integral_constant<int, 0>;
@@ -238,20 +267,16 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         }
         if (j < P)
             step(X, Y, j, K2{}, W0{}, CR{});
-        // border rows of the image: first row +1, last row -1 (its down pairs
-        // were emitted as equal fakes: the down row was the row itself)
-        if (__any_sync(0xFFFFFFFFu, G.nrows > 0 && (G.y0 == 0 || G.y0 + G.nrows == p.h))) {
-            const int nreal = ALIGNED ? 16 : min(16, G.e + 1);
-            if (G.nrows > 0 && G.y0 == 0) {
-                const uint8_t* rp = G.p + p.pitch;
-                for (int i = 0; i < nreal; ++i)
-                    red_add(corr_g + ((uint32_t)rp[i] << 2), 1u);
-            }
-            if (G.nrows > 0 && G.y0 + G.nrows == p.h) {
-                const uint8_t* rp = G.p + (size_t)G.nrows * p.pitch;
-                for (int i = 0; i < nreal; ++i)
-                    red_add(corr_g + ((uint32_t)rp[i] << 2), 0xFFFFFFFFu);
-            }
+        // the image's last row (its down pairs were emitted as equal fakes:
+        // the down row was the row itself): corr -1 per pixel.  It was the
+        // row processed at position P - 1 (C of that step: Y if P - 1 is
+        // even, else X); outside the walk loop, which stays branch-free.
+        if (G.nrows > 0 && G.y0 + G.nrows == p.h) {
+            const Car& Cl = ((P - 1) & 1) ? X : Y;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (ALIGNED || i <= G.e)
+                    corr_add(Cl.A[i], 0xFFFFFFFFu);
         }
         __syncthreads();
         TWCYC(0);  // walk (incl. the wait for the slowest warp)
@@ -262,69 +287,80 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         if constexpr (LG == 4) {
             // Cooperative flush for 8 images per round (C5): warp w owns the
             // keys [16 w, 16 w + 16) of all 8 images; lane L takes image
-            // L & 7, keys t0 .. t0 + 3 (t0 = 16 w + 4 (L >> 3)).  A group's 4
-            // lane words of a counter row are one 16-byte piece, and the 8
-            // lanes of a quarter warp (one LDS.128 wavefront) hit 8 bank quads, so
-            // the counters are read once, conflict free, straight into the
-            // per-image combinations; the scans run across the 4 lanes of an
-            // image and then across warps (two small carry exchanges).  No
-            // transposed scratch copy, no second clearing pass.
-            // (the 8 lanes of each quarter warp -- one LDS.128 wavefront --
-            // take 8 different images, i.e. 8 different bank quads)
+            // gi = L & 7, keys t0 .. t0 + 3 (t0 = 16 w + 4 (L >> 3)) of the W
+            // table and rows 2 t0 .. 2 t0 + 7 of the Hs table.  A group's 4
+            // lane words of a counter row are one 16-byte piece and the 8
+            // lanes of a quarter warp (one LDS.128 wavefront) take 8 images,
+            // i.e. 8 bank quads: conflict free.  Every piece has exactly one
+            // reader, which clears it right after reading (no second pass).
+            // The reconstruction of keys t0.. also needs the last key / the
+            // last three Hs rows of the previous owner: a shuffle from lane
+            // L - 8, or for the first quarter warp from warp w - 1 through
+            // shared memory.
             const int gi = lane & 7, q4 = lane >> 3;
             const int t0 = 16 * warp + 4 * q4;
-            auto grp = [&](int row, int half) -> uint4 {
-                return *reinterpret_cast<const uint4*>(hist + row * 256 + half * 128 + gi * 16);
-            };
-            auto wsum = [](const uint4& v, long long& h, long long& b) {
-                h += (long long)((v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu));
-                b += (long long)((v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16));
-            };
-            long long hv[5] = {0, 0, 0, 0, 0};  // hist(t0 - 1 + i)
-            long long cd[4], h2[4];
-#pragma unroll
-            for (int i = 0; i < 5; ++i) {
-                const int t = t0 - 1 + i;
-                long long hh = 0, bb = 0;
-                if (t >= 0) {
-                    wsum(grp(t, 1), hh, bb);        // W copy 0
-                    wsum(grp(256 + t, 1), hh, bb);  // W copy 1
-                }
-                hv[i] = hh;
-                if (i > 0)
-                    cd[i - 1] = bb - 4ll * hh;
-            }
-            long long hs[9];  // Hs rows 2 t0 - 3 .. 2 t0 + 5
-#pragma unroll
-            for (int i = 0; i < 9; ++i) {
-                const int r = 2 * t0 - 3 + i;
-                long long v = 0;
-                if (r >= 0) {
-                    const uint4 c = grp(r, 0);
-                    v = (long long)c.x + c.y + c.z + c.w;
-                }
-                hs[i] = v;
-            }
-            const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + gi * 1024);
+            uint32_t hh[4], bb[4];  // hist(t0 + i), B sums
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int u = t0 + i;  // h2(u) = 4 hist(u-1) - corr(u-1) - hs(2u-3) - 2 hs(2u-2) - hs(2u-1)
-                h2[i] = u == 0 ? 0
-                               : 4ll * hv[i] - (long long)cr[u - 1] - hs[2 * i] - 2ll * hs[2 * i + 1] -
-                                     hs[2 * i + 2];
+                uint4* c = reinterpret_cast<uint4*>(hist + (t0 + i) * 256 + 128 + gi * 16);
+                const uint4 v = *c;
+                *c = make_uint4(0, 0, 0, 0);
+                hh[i] = (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
+                bb[i] = (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
             }
-            // hs[0] (row 2 t0 - 3) is counted for u = t0 only when u >= 2: a
-            // negative row is 0 already, so the formula matches warp_curve256_regs'
-            uint32_t hist_keep[4];
+            uint32_t hs[8];  // Hs rows 2 t0 + i (row 511 is the dummy row: cleared, not counted)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = 2 * t0 + i;
+                uint4* c = reinterpret_cast<uint4*>(hist + r * 256 + gi * 16);
+                const uint4 v = *c;
+                *c = make_uint4(0, 0, 0, 0);
+                hs[i] = r < 511 ? v.x + v.y + v.z + v.w : 0u;
+            }
+            int crv[4];  // corr(t0 + i): the lane-striped second W copy
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint4* c = reinterpret_cast<uint4*>(hist + (256 + t0 + i) * 256 + 128 + gi * 16);
+                const uint4 v = *c;
+                *c = make_uint4(0, 0, 0, 0);
+                crv[i] = (int)(v.x + v.y + v.z + v.w);
+            }
+            // previous owner's hist(t0 - 1), Hs rows 2 t0 - 3 .. 2 t0 - 1, corr(t0 - 1)
+            uint32_t ph = __shfl_up_sync(0xFFFFFFFFu, hh[3], 8);
+            uint32_t pa = __shfl_up_sync(0xFFFFFFFFu, hs[5], 8);
+            uint32_t pb = __shfl_up_sync(0xFFFFFFFFu, hs[6], 8);
+            uint32_t pc = __shfl_up_sync(0xFFFFFFFFu, hs[7], 8);
+            int pcr = __shfl_up_sync(0xFFFFFFFFu, crv[3], 8);
+            uint4* xch = reinterpret_cast<uint4*>(sm + Lay::kXch);
+            int* xchc = reinterpret_cast<int*>(sm + Lay::kXchC);
+            if (q4 == 3) {
+                xch[warp * 8 + gi] = make_uint4(hh[3], hs[5], hs[6], hs[7]);
+                xchc[warp * 8 + gi] = crv[3];
+            }
+            __syncthreads();
+            if (q4 == 0) {
+                if (warp > 0) {
+                    const uint4 x = xch[(warp - 1) * 8 + gi];
+                    ph = x.x;
+                    pa = x.y;
+                    pb = x.z;
+                    pc = x.w;
+                    pcr = xchc[(warp - 1) * 8 + gi];
+                } else {
+                    ph = pa = pb = pc = 0u;
+                    pcr = 0;
+                }
+            }
+            long long cd[4], h2[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                hist_keep[i] = (uint32_t)hv[i + 1];
-            __syncthreads();  // every counter read: clear the block for the next round
-            {
-                uint4* z = reinterpret_cast<uint4*>(hist);
-                for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
-                    z[i] = make_uint4(0, 0, 0, 0);
-            }
+                cd[i] = (long long)bb[i] - 4ll * (long long)hh[i];
+            // h2(u) = 4 hist(u-1) - corr(u-1) - hs(2u-3) - 2 hs(2u-2) - hs(2u-1), u = t0 + i
+            h2[0] = t0 == 0 ? 0
+                            : 4ll * ph - (long long)pcr - (long long)pa - 2ll * pb - (long long)pc;
+            h2[1] = 4ll * hh[0] - (long long)crv[0] - (long long)pc - 2ll * hs[0] - (long long)hs[1];
+            h2[2] = 4ll * hh[1] - (long long)crv[1] - (long long)hs[1] - 2ll * hs[2] - (long long)hs[3];
+            h2[3] = 4ll * hh[2] - (long long)crv[2] - (long long)hs[3] - 2ll * hs[4] - (long long)hs[5];
             // scans: lane-local, then across the image's 4 lanes (a quad)
             long long* tot = reinterpret_cast<long long*>(sm + Lay::kTot);  // [3][16][NG]
             auto quad_scan = [&](long long (&v)[4]) -> long long {
@@ -370,23 +406,23 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 cs += tot[(2 * 16 + w2) * NG + gi];
             const long long im = i0 + gi;
             if (im < p.n) {
+                // 64-bit stores straight from the register pairs: STG.128 made
+                // ptxas funnel all four through one register quad, each waiting
+                // for the previous store to release it (long-scoreboard stalls)
                 uint64_t* os = p.sums + (size_t)im * 256 + t0;
                 uint64_t* oc = p.cards + (size_t)im * 256 + t0;
-                *reinterpret_cast<ulonglong2*>(oc) = make_ulonglong2((uint64_t)cd[0], (uint64_t)cd[1]);
-                *reinterpret_cast<ulonglong2*>(oc + 2) = make_ulonglong2((uint64_t)cd[2], (uint64_t)cd[3]);
-                *reinterpret_cast<ulonglong2*>(os) =
-                    make_ulonglong2((uint64_t)(h2[0] + cs), (uint64_t)(h2[1] + cs));
-                *reinterpret_cast<ulonglong2*>(os + 2) =
-                    make_ulonglong2((uint64_t)(h2[2] + cs), (uint64_t)(h2[3] + cs));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    oc[i] = (uint64_t)cd[i];
+                    os[i] = (uint64_t)(h2[i] + cs);
+                }
                 if (p.hist_out) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        p.hist_out[(size_t)im * 256 + t0 + i] = hist_keep[i];
+                        p.hist_out[(size_t)im * 256 + t0 + i] = hh[i];
                 }
             }
             TWCYC(1);
-            for (int i = tid; i < NG * 256; i += kTwThreads)
-                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         } else
         {
             // 1. every thread: 2*NG (half-row, group) cells, contiguous 16-byte
@@ -443,7 +479,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 const uint32_t* b0 = h0 + kTwArr;
                 const uint32_t* h1 = b0 + kTwArr;
                 const uint32_t* b1 = h1 + kTwArr;
-                const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + warp * 1024);
+                const int* cr = reinterpret_cast<const int*>(sm + Lay::kCorr + warp * kTwCorrStride);
                 auto histv = [&](int v) { return (long long)h0[pad8(v)] + (long long)h1[pad8(v)]; };
                 auto hs = [&](int s) { return (long long)base[pad16(s)]; };
                 uint64_t card[8], sum[8];
@@ -481,7 +517,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             uint4* z = reinterpret_cast<uint4*>(hist);
             for (int i = tid; i < NG * kTwImgWords / 4; i += kTwThreads)
                 z[i] = make_uint4(0, 0, 0, 0);
-            for (int i = tid; i < NG * 256; i += kTwThreads)
+            for (int i = tid; i < NG * (int)(kTwCorrStride / 4); i += kTwThreads)
                 reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
         __syncthreads();

@@ -371,7 +371,9 @@ int launch_twalk_t(const TwParams& tp, unsigned G, cudaStream_t stream)
 // K5 geometry for a batch of n w x h images: the smallest lane group LG (most
 // images per round) whose 16 * LG walkers cover the image with walks of
 // R <= 62 rows (a W lane word takes <= 16 warps * (R/2 + 1) * 16 <= 8191
-// events per round).  Returns false when no LG fits (K1 is used instead).
+// events per round with two W copies; LG = 4 keeps one W copy, so R <= 31
+// there: 16 * 31 * 16 <= 8191).  Returns false when no LG fits (K1 is used
+// instead).
 bool twalk_geometry(int n, int w, int h, int& lg, int& R, int& C)
 {
     const int S = (w + 15) / 16;
@@ -383,7 +385,7 @@ bool twalk_geometry(int n, int w, int h, int& lg, int& R, int& C)
             continue;
         const int c = walkers / S;
         const int r = (h + c - 1) / c;
-        if (r > 62)
+        if (r > (cand == 4 ? 31 : 62))
             continue;
         lg = cand;
         R = r;

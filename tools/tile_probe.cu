@@ -9,9 +9,30 @@ int main(int argc, char** argv)
               h = argc > 3 ? atoi(argv[3]) : 128;
     kohler_cuda_ctx* ctx = nullptr;
     if (kohler_cuda_create(0, &ctx)) { printf("%s\n", kohler_cuda_last_error()); return 1; }
+    const int fam = argc > 4 ? atoi(argv[4]) : 0;  // 1: the four C5 families by i mod 4
     std::vector<uint8_t> img((size_t)n * w * h);
     uint32_t x = 1;
-    for (auto& v : img) { x = x * 1664525u + 1013904223u; v = (uint8_t)(x >> 24); }
+    auto rnd = [&]() { x = x * 1664525u + 1013904223u; return x >> 8; };
+    if (!fam) {
+        for (auto& v : img) v = (uint8_t)(rnd() >> 16);
+    } else {
+        for (int i = 0; i < n; ++i) {
+            uint8_t* im = img.data() + (size_t)i * w * h;
+            const int f = i & 3, cell = 1 + (int)(rnd() % 8), cval = (int)(rnd() % 256);
+            int band = 0, left = 0;
+            for (int yy = 0; yy < h; ++yy) {
+                if (f == 0 && left-- <= 0) { band = (int)(rnd() % 3); left = 1 + (int)(rnd() % 20); }
+                for (int xx = 0; xx < w; ++xx) {
+                    int v;
+                    if (f == 0) v = band == 0 ? 0 : band == 1 ? 128 : 255;
+                    else if (f == 1) v = cval;
+                    else if (f == 2) v = ((xx / cell + yy / cell) & 1) ? 255 : 0;
+                    else { const int s = (int)(rnd() % 31) - 15 + (int)(rnd() % 31) - 15; v = ((rnd() & 1) ? 60 : 190) + s / 2; }
+                    im[(size_t)yy * w + xx] = (uint8_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+                }
+            }
+        }
+    }
     uint8_t* d; cudaMalloc(&d, img.size()); cudaMemcpy(d, img.data(), img.size(), cudaMemcpyHostToDevice);
     uint64_t* sums; cudaMalloc(&sums, (size_t)n * 4096);
     int* ints; cudaMalloc(&ints, (size_t)n * 64);
