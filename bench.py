@@ -12,9 +12,9 @@ one pass of that pipeline over the image.
 --gpus N > 1 without torchrun: the script relaunches itself under
 ``torch.distributed.run`` with N processes (one per GPU, NCCL, 127.0.0.1).
 
-N = 1: per step one K1 launch (accumulate) and one finish launch (K3
-reconstruct + K4 select), PDL-chained; pipeline depth 3 (three steps in
-flight on a third of the SMs each).
+N = 1: per step one K1 launch: the walk accumulates, and the CTA whose flush
+lands last runs K3 (reconstruct) + K4 (select); PDL-chained; pipeline depth
+3 (three steps in flight on a third of the SMs each).
 N > 1: the image is split into row bands with a one-row halo
 (proj/src/fast.cpp:42-57); per step each rank runs K1 on its band, the 512
 u64 partials of 8 steps are merged by one NCCL all-reduce (asynchronous,
@@ -404,8 +404,8 @@ def main():
         def step(i):
             ctx.analyze_batch_device(buf[i % copies], w, h, pitch, img_bytes, 1, K_TOP, out)
         drain = None
-        launches_per_step = None  # counted after the first step (K1 walk + K3/K4 finish)
-        parallel = ("1 GPU, K1 walk + K3/K4 finish per step (PDL-chained)"
+        launches_per_step = None  # counted after the first step (one K1: walk + in-CTA K3/K4)
+        parallel = ("1 GPU, one K1 per step (walk; K3/K4 by its last-flushing CTA; PDL-chained)"
                     + (f"; {args.depth} steps in flight, K1 on 1/{args.depth} of the SMs each "
                        "(kohler_cuda_set_pipeline_depth)" if args.depth > 1 else ""))
     else:
@@ -431,7 +431,7 @@ def main():
                 # first band kernel) one selection launch for the previous m
                 ba.step_bucketed(buf[i % copies], pitch)
             drain = ba.drain_buckets
-            launches_per_step = 2 + 1.0 / bucket  # band K1 + finish per step, a select per bucket
+            launches_per_step = 1 + 1.0 / bucket  # band K1 (self-finishing) per step, a select per bucket
             parallel = (f"row bands x{world} + 1-row halo; NCCL all-reduce of the 512 u64 partials "
                         f"of {bucket} steps at once (async, overlapped with the next bucket's band "
                         "kernels), one selection launch per bucket; strong scaling")
@@ -441,7 +441,7 @@ def main():
             def step(i):
                 ba.step_pipelined(i, buf[i % copies], pitch)
             drain = ba.drain
-            launches_per_step = 3  # band K1 + finish, select
+            launches_per_step = 2  # band K1 (self-finishing), select
             parallel = (f"row bands x{world} + 1-row halo, NCCL all-reduce of 512 u64 overlapped "
                         "with the next step's band kernel, strong scaling")
 
@@ -600,7 +600,7 @@ def main():
                        "pipeline_depth": args.depth if not bands else args.band_depth},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "walk_kernel<true> (K1; finish_kernel K3/K4 PDL-overlapped)" if not bands
+                         "kernel": "walk_kernel<true> (K1; K3/K4 in its last-flushing CTA)" if not bands
                          else "walk_kernel<true> band partial (K1)",
                          "algorithmic_bytes_per_launch": kbytes, "kernel_ms": kern_ms,
                          "peak_source": peak_src},
@@ -852,7 +852,7 @@ def measure_e2e_bands(ba, img, args, dev, pitch):
 
 def measure_e2e(ctx, img, args, dev_index):
     """Same metric through the public host C ABI, every step: the image from
-    pinned host memory -> H2D -> K1 + finish -> D2H of curve, mean curve and
+    pinned host memory -> H2D -> K1 (+ K3/K4) -> D2H of curve, mean curve and
     thresholds.  Headline: the streaming API (kohler_cuda_submit /
     kohler_cuda_collect, two steps in flight, so step i + 1's upload runs
     under step i's kernels); also reported: the synchronous

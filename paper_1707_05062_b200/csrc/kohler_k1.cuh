@@ -89,6 +89,123 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishParams p)
     }
 }
 
+// K3 + K4 inside K1 for single-image launches, from the image's 512 exact
+// combinations in shared memory (sval, at kSmVal; the scratch aliases the
+// idle row ring).  Same arithmetic as finish_kernel.  Called by every thread
+// of one CTA.  Waits for the previous launch (griddepcontrol.wait) right
+// before the first output store only: calls reusing the output buffers stay
+// in stream order, everything before the stores overlaps the predecessor.
+__device__ void finish_from_vals(const WideParams& p, int img, unsigned char* sm)
+{
+    const int tid = threadIdx.x;
+    long long* sval = reinterpret_cast<long long*>(sm + kSmVal);
+    uint64_t* ccard = reinterpret_cast<uint64_t*>(sm + kSmCurve);
+    uint64_t* csum = ccard + 256;
+    double* mean = reinterpret_cast<double*>(sm + kSmMean);
+    uint8_t* def = sm + kSmDef;
+    unsigned char* scr = sm + kSmScratch;                           // block_select256: 3136 B
+    long long* tmp = reinterpret_cast<long long*>(scr + 3200);      // [256]
+    const int warp = tid >> 5;
+    if (warp == 0)
+        warp_prefix256(sval, reinterpret_cast<long long*>(ccard));
+    else if (warp == 1) {
+        warp_prefix256(sval + 256, tmp);
+        __syncwarp();
+        warp_prefix256(tmp, reinterpret_cast<long long*>(csum));
+    }
+    __syncthreads();
+    if (tid < 256) {
+        const uint64_t cs = csum[tid], cc = ccard[tid];
+        mean[tid] = cc ? (double)cs / (double)cc : 0.0;
+        def[tid] = cc ? 1 : 0;
+    }
+    pdl_wait();
+    if (tid < 256) {
+        const uint64_t cs = csum[tid], cc = ccard[tid];
+        if (p.sums)
+            p.sums[(size_t)img * 256 + tid] = cs;
+        if (p.cards)
+            p.cards[(size_t)img * 256 + tid] = cc;
+        if (p.values)
+            p.values[(size_t)img * 256 + tid] = mean[tid];
+        if (p.defined)
+            p.defined[(size_t)img * 256 + tid] = def[tid];
+    }
+    __syncthreads();
+    if (p.select && tid < 256) {
+        const int st = block_select256(mean, def, p.k, scr, 1, p.t0s ? p.t0s + img : nullptr,
+                                       p.topks ? p.topks + (size_t)img * p.k : nullptr,
+                                       p.topk_counts ? p.topk_counts + img : nullptr);
+        if (tid == 0 && p.status)
+            p.status[img] = st;
+    }
+    __syncthreads();
+}
+
+// Ticket variant (self_finish): the CTA whose flush landed last reads the
+// image's accumulator copies (summed, reset: self-cleaning), then K3 + K4.
+__device__ void finish_in_cta(const WideParams& p, int img, unsigned char* sm)
+{
+    long long* sval = reinterpret_cast<long long*>(sm + kSmVal);
+    for (int r = threadIdx.x; r < 512; r += kWalkThreads) {
+        unsigned long long* a = p.acc + (size_t)img * p.copies * 512 + r;
+        unsigned long long v[kAccCopiesSingle];
+#pragma unroll
+        for (int c = 0; c < kAccCopiesSingle; ++c)
+            v[c] = c < p.copies ? __ldcg(a + c * 512) : 0ull;
+        unsigned long long s = 0;
+#pragma unroll
+        for (int c = 0; c < kAccCopiesSingle; ++c) {
+            s += v[c];
+            if (c < p.copies)
+                __stcg(a + c * 512, 0ull);
+        }
+        sval[r] = (long long)s;
+    }
+    if (threadIdx.x == 0)
+        p.tickets[img] = 0u;  // self-cleaning for the next call
+    __syncthreads();
+    finish_from_vals(p, img, sm);
+}
+
+// Cluster variant (small single images: the grid is one thread-block
+// cluster, <= 8 CTAs): every CTA left its 512 combinations in its own
+// shared memory (kSmVal); CTA rank 0 sums them over distributed shared
+// memory and finishes.  No global accumulator, no ticket, no dependency on
+// the previous launch until the output stores.
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ void finish_cluster(const WideParams& p, int img, unsigned char* sm)
+{
+    cluster_sync_all();  // every CTA's combinations are in its shared memory
+    unsigned rank, nranks;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nranks));
+    long long* sval = reinterpret_cast<long long*>(sm + kSmVal);
+    if (rank == 0) {
+        for (int t = threadIdx.x; t < 512; t += kWalkThreads) {
+            const uint32_t la = (uint32_t)__cvta_generic_to_shared(sval + t);
+            long long s = sval[t];
+            for (unsigned r = 1; r < nranks; ++r) {
+                uint32_t ra;
+                long long v;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
+                asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+                s += v;
+            }
+            sval[t] = s;
+        }
+    }
+    cluster_sync_all();  // the peers' shared memory stays valid until rank 0 has read it
+    if (rank == 0) {
+        __syncthreads();
+        finish_from_vals(p, img, sm);
+    }
+}
+
 // Fold the packed W words (both copies) into the u64 per-CTA accumulators
 // and clear them.  Thread t owns (copy t >> 8, key t & 255): 32 lane words
 // read rotated by t & 7 so a warp's LDS.128 hit distinct bank quads.
@@ -257,7 +374,10 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
     KCYC(6);
     phase(9);
     // the accumulators may still be read / reset by the previous finish_kernel
-    pdl_wait();
+    // (cluster mode: no shared workspace, the finishing CTA waits before its
+    // output stores instead)
+    if (!p.cluster)
+        pdl_wait();
     phase(10);
     for (int t = tid; t < 512; t += kWalkThreads) {
         auto hist = [&](int v) { return (long long)(wacc[v] + wacc[512 + v] + hb[v]); };
@@ -276,7 +396,9 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
                     val -= (long long)hs_tot[2 * u - 3];
             }
         }
-        if (val != 0) {
+        if (p.cluster) {
+            reinterpret_cast<long long*>(sm + kSmVal)[t] = val;
+        } else if (val != 0) {
             const int copy = blockIdx.x % p.copies;
             atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + t, (unsigned long long)val);
         }
@@ -543,7 +665,7 @@ __device__ __forceinline__ void zero_counters(unsigned char* sm, unsigned char* 
         reinterpret_cast<uint32_t*>(sm + kSmHb)[i] = 0;
 }
 
-template <bool ALIGNED, bool TWO_W, bool RGB>
+template <bool ALIGNED, bool TWO_W, bool RGB, bool CL>
 __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* sm,
                                            unsigned char* hist, uint32_t smbase,
                                            const uint8_t* base, long long ua, long long ub,
@@ -553,12 +675,19 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane4 = (uint32_t)lane * 4u;
+    // cluster launches: every .shared::cta address carries the CTA rank in
+    // bits 24+ (as cvta returns it); the counter addresses get it from the
+    // per-lane byte source of the address PRMT (absorb), so the fixed
+    // immediates stay
+    const uint32_t rbits = CL ? (smbase & 0xFF000000u) : 0u;
+    const uint32_t lane_ra = lane4 | rbits;
     using F = K1Fmt<RGB>;
     constexpr uint32_t HA = F::hist_abs;
-    const uint32_t kneg = HA - lane4;  // pair event at A_a + A_b + kneg
-    const uint32_t dummy = HA + kDummy + lane4;
-    // corr[v] of a pixel with W address A: corr_base + (A >> 6) (A >> 6 = 4v + (lane4 >> 6))
-    const uint32_t corr_base = smbase + F::shift + kSmCorr - (lane4 >> 6);
+    const uint32_t kneg = HA - lane4 - rbits;  // pair event at A_a + A_b + kneg
+    const uint32_t dummy = HA + kDummy + lane4 + rbits;
+    // corr[v] of a pixel with W address A: corr_base + (A >> 6)
+    // (A >> 6 = (rbits >> 6) + 4v + (lane4 >> 6); smbase carries rbits)
+    const uint32_t corr_base = smbase + F::shift + kSmCorr - (lane4 >> 6) - (rbits >> 6);
     const int R = p.R;
     const uint32_t pitch = (uint32_t)p.pitch;  // < 2^32 (checked by the host)
     const bool any = ua < ub;
@@ -651,7 +780,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 fetch_row<RGB>(N, j + AH - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
-            absorb<ALIGNED>(D, r, lane4, G.e);
+            absorb<ALIGNED>(D, r, lane_ra, G.e);
             if (KIND == 1) {
                 // prime: q(up -> row r0) from row r0 - 1 (neutral at the band's first row)
                 const bool has_up = G.y0 + r0 > 0;
@@ -672,7 +801,7 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
                 D.ue[jj] = qde[jj];
                 D.uo[jj] = qdo[jj];
             }
-            const uint32_t Arn = __byte_perm(C.rn, lane4, 0x5504);
+            const uint32_t Arn = __byte_perm(C.rn, lane_ra, 0x7604);
             if (ALIGNED || !F.ragged) {
                 if (live) {
 #pragma unroll
@@ -738,16 +867,22 @@ __device__ __forceinline__ void walk_range(const WideParams& p, unsigned char* s
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <bool ALIGNED, bool TWO_W, bool RGB>
+template <bool ALIGNED, bool TWO_W, bool RGB, bool CL = false>
 __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_constant__ WideParams p)
 {
     using F = K1Fmt<RGB>;
     extern __shared__ __align__(16) unsigned char sm_dyn[];
+    // Shared address of the dynamic block.  In a cluster launch it carries the
+    // CTA rank in bits 24+ (measured: rank r -> (r << 24) | 0x400, for
+    // cvta.to.shared and cvta.to.shared::cta alike), and every .shared::cta
+    // access must too (walk_range adds the rank bits to the counter
+    // addresses); smloc is the offset inside the CTA's window.
     const uint32_t smbase = (uint32_t)__cvta_generic_to_shared(sm_dyn);
-    if (smbase + F::shift + kSmMiscEnd > F::hist_abs ||
-        F::hist_abs + kohler_walk::kHistBytes > smbase + F::smem)
+    const uint32_t smloc = smbase & 0x00FFFFFFu;
+    if (smloc + F::shift + kSmMiscEnd > F::hist_abs ||
+        F::hist_abs + kohler_walk::kHistBytes > smloc + F::smem)
         __trap();  // the fixed counter address would overlap the scratch (never seen)
-    unsigned char* hist = sm_dyn + (F::hist_abs - smbase);
+    unsigned char* hist = sm_dyn + (F::hist_abs - smloc);
     // the scratch block (all kSm* offsets below), above the ring
     unsigned char* sm = sm_dyn + F::shift;
     const int tid = threadIdx.x;
@@ -794,7 +929,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
                 const long long n = eb - ea;
                 const long long wa = ea + n * warp / kWalkWarps;
                 const long long wb = ea + n * (warp + 1) / kWalkWarps;
-                walk_range<ALIGNED, TWO_W, RGB>(p, sm, hist, smbase, base, wa, wb, !zeroed);
+                walk_range<ALIGNED, TWO_W, RGB, CL>(p, sm, hist, smbase, base, wa, wb, !zeroed);
                 warp_end();
                 zeroed = true;
                 __syncthreads();
@@ -812,6 +947,21 @@ __global__ void __launch_bounds__(kWalkThreads, 1) walk_kernel(const __grid_cons
             flush_image<RGB>(ps, img, sm, hist, img < i_last, TWO_W, prefetched && img == i_first, img == i_first);
             // (the last image: no re-zeroing)
             flushed = true;
+            if (CL) {
+                finish_cluster(ps, img, sm);
+            } else if (ps.self_finish) {
+                // ticket: the CTA whose REDGs land last finishes the image
+                __threadfence();
+                __syncthreads();
+                int* flag = reinterpret_cast<int*>(sm + kSmFlag);
+                if (tid == 0)
+                    *flag = atomicAdd(ps.tickets + img, 1u) == gridDim.x - 1u;
+                __syncthreads();
+                if (*flag) {
+                    __threadfence();
+                    finish_in_cta(ps, img, sm);
+                }
+            }
         }
     }
     if (!flushed)

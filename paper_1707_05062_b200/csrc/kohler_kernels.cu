@@ -72,6 +72,8 @@ struct WideParams {
     int select;
     int no_finish;  // accumulate only (a band of a chunked image; a later launch finishes)
     int early_trigger;  // pipelined launches: let the next launch start at once (disjoint SMs)
+    int self_finish;    // single-image launch: the CTA that flushes last runs K3 + K4 (no finish_kernel)
+    int cluster;        // single small image: the grid is one cluster, reduced over DSMEM (no accumulator)
     uint32_t* hist_out;  // [n][256] pixel histogram (atomically accumulated), or null
     uint64_t* sums;
     uint64_t* cards;
@@ -122,6 +124,7 @@ constexpr uint32_t kSmHb = (kSmBorder + 3 * kBorderRow + 15) & ~15u;  // u32 [2]
 // has lost them to the walk's instruction stream (each cold LDC cost ~0.25 us)
 constexpr uint32_t kSmParams = kSmHb + 2048;
 constexpr uint32_t kSmBslice = kSmParams + 256;  // BorderSlice of the CTA's first image
+constexpr uint32_t kSmFlag = kSmBslice + 12;     // int: this CTA finishes the image (self_finish)
 constexpr uint32_t kSmMiscEnd = kSmBslice + 16;
 constexpr uint32_t kSmVal = kSmRing;                 // i64[512]
 constexpr uint32_t kSmCurve = kSmVal + 4096;         // u64 sum[256], card[256]
@@ -342,6 +345,7 @@ struct kohler_cuda_ctx {
     int last_grid = 0;  // grid of the last K1 launch (debug tools)
     int depth = 1;      // K1 launches in flight (kohler_cuda_set_pipeline_depth)
     bool rgb_fused = true;  // K1 reads RGB itself where the layout allows (env KOHLER_RGB_UNFUSED=1: off)
+    bool no_cluster = false;  // env KOHLER_NO_CLUSTER=1: small single images take the ticket path (A/B, tests)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };
@@ -378,6 +382,8 @@ int kohler_cuda_create(int device, kohler_cuda_ctx** out)
     {
         const char* e = std::getenv("KOHLER_RGB_UNFUSED");
         ctx->rgb_fused = !(e && e[0] && e[0] != '0');
+        const char* c = std::getenv("KOHLER_NO_CLUSTER");
+        ctx->no_cluster = c && c[0] && c[0] != '0';
     }
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);

@@ -136,6 +136,8 @@ cudaError_t launch_pdl(Kern kernel, unsigned grid, unsigned block, size_t smem, 
 #define KOHLER_SINGLE_W 0
 #endif
 constexpr bool kSingleW = KOHLER_SINGLE_W != 0;
+constexpr long long kClusterMax = 8;     // portable cluster size
+constexpr long long kSelfFinishMax = 24;
 
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
@@ -241,6 +243,19 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     p.k = k;
     p.select = select;
     p.no_finish = no_finish;
+    // One image per launch: small grids (<= 8 CTAs) run as ONE thread-block
+    // cluster whose rank-0 CTA sums the CTAs' combinations over distributed
+    // shared memory and finishes (no global accumulator, so consecutive
+    // launches share no workspace and overlap freely, stream order kept by the
+    // griddepcontrol.wait before the output stores); mid-size grids let the
+    // CTA whose flush lands last finish (ticket); larger ones keep
+    // finish_kernel, which runs on the SM the pipelined K1s leave free.
+    const bool single = n == 1 && !no_finish;
+    // (two W copies: the cluster kernels are instantiated for that layout only)
+    p.cluster = (single && G <= kClusterMax && !ctx->no_cluster && !rgb && two_w) ? 1 : 0;
+    p.self_finish = (single && !p.cluster && G <= kSelfFinishMax) ? 1 : 0;
+    if (p.cluster)
+        p.early_trigger = 1;
     p.hist_out = hist_out;
     p.sums = o.sums;
     p.cards = o.cards;
@@ -290,6 +305,10 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytesRgb));
         KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, false, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytesRgb));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<false, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
         ctx->wide_attr_set = true;
     }
     ctx->last_grid = (int)G;
@@ -298,12 +317,19 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     cfg.blockDim = dim3(kWalkThreads);
     cfg.dynamicSmemBytes = rgb ? kSmWideBytesRgb : kSmWideBytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)G;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (rgb)
+    cfg.numAttrs = p.cluster ? 2 : 1;
+    if (p.cluster)
+        KC_CUDA(w % 16 == 0 ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true, false, true>, p)
+                            : cudaLaunchKernelEx(&cfg, walk_kernel<false, true, false, true>, p));
+    else if (rgb)
         KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<true, true, true>, p)
                       : cudaLaunchKernelEx(&cfg, walk_kernel<true, false, true>, p));
     else if (w % 16 == 0)
@@ -313,7 +339,7 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         KC_CUDA(two_w ? cudaLaunchKernelEx(&cfg, walk_kernel<false, true, false>, p)
                       : cudaLaunchKernelEx(&cfg, walk_kernel<false, false, false>, p));
     ctx->last_launches += 1;
-    if (!no_finish) {
+    if (!no_finish && !p.self_finish && !p.cluster) {
         FinishParams fp{};
         fp.acc = p.acc;
         fp.copies = copies;

@@ -39,8 +39,10 @@
 //   rows of 256 B, word (row, half, lane) at row*256 + half*128 + lane*4
 //   half 0, rows 0..510 : Hs[s];  row 511: dummy (neutralised events)
 //   half 1, rows 0..255 : W copy 0 (even rows);  rows 256..511: W copy 1 (odd rows)
-// A pixel's W address is A = (v << 8) | lane*4 (one PRMT); a pair's Hs
-// address is A_a + A_b - lane*4 = (a + b) << 8 | lane*4 (one IADD3).
+// A pixel's W address is A = (v << 8) | lane*4 (one PRMT; bytes 2 and 3 come
+// from the same byte source as lane*4: the CTA rank bits of a cluster
+// launch, else 0); a pair's Hs address is A_a + A_b - lane*4 - rank bits =
+// (a + b) << 8 | lane*4 | rank bits (one IADD3).
 #pragma once
 
 #include <cstdint>
@@ -132,7 +134,7 @@ __device__ __forceinline__ void absorb(Car& Y, const Row& r0, uint32_t lane4, in
         Y.o[j] = __byte_perm(r.w[j], kTo, 0x4341);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            Y.A[4 * j + k] = __byte_perm(r.w[j], lane4, 0x5504 | (k << 4));
+            Y.A[4 * j + k] = __byte_perm(r.w[j], lane4, 0x7604 | (k << 4));
     }
     Y.ln = r.ln;
     Y.rn = r.rn;

@@ -36,7 +36,7 @@ def test_device_line_keys():
     assert c and c["kind"] == "reference" and c["value"] > 0 and c["cores"] >= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 5184 * 3456 and e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] >= 2 * 120
+    assert d["gpu_launches"] >= 120
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
 
 

@@ -95,10 +95,12 @@ def test_fused_rgb_vs_oracle(ctx, unfused, orc, w, h, n, kind, pp, ps):
     rng = np.random.default_rng(w * 7919 + h * 31 + n)
     rgb = np.stack([_image(rng, h, w, kind) for _ in range(n)])
     out, launches = _run(ctx, rgb, pp, ps)
-    assert launches == 2  # K1 over RGB + finish: no luma_kernel, no grey image
+    # K1 over RGB (+ finish_kernel unless the single-image K1 finishes itself):
+    # no luma_kernel, no grey image
+    assert launches in ((1, 2) if n == 1 else (2,))
     _check(out, orc, rgb)
     out2, launches2 = _run(unfused, rgb, pp, ps)
-    assert launches2 == 3  # luma_kernel + K1 + finish
+    assert launches2 == launches + 1  # + luma_kernel
     for key in ("sums", "cards", "values", "t0", "topk", "topk_count", "status"):
         assert torch.equal(out[key], out2[key]), key
 
@@ -109,11 +111,11 @@ def test_fused_rgb_layouts_that_take_the_two_pass_path(ctx, orc):
     rng = np.random.default_rng(5)
     rgb = rng.integers(0, 256, (1, 40, 100, 3), dtype=np.uint8)  # w % 16 != 0
     out, launches = _run(ctx, rgb)
-    assert launches == 3
+    assert launches in (2, 3)  # luma_kernel + K1 (+ finish_kernel)
     _check(out, orc, rgb)
     rgb = rng.integers(0, 256, (1, 40, 96, 3), dtype=np.uint8)
     out, launches = _run(ctx, rgb, pad_pitch=8)  # pitch % 16 != 0
-    assert launches == 3
+    assert launches in (2, 3)
     _check(out, orc, rgb)
 
 
@@ -142,8 +144,10 @@ def test_fused_rgb_host_path(ctx, unfused, orc, w, h, n):
     rng = np.random.default_rng(w + h + n)
     rgb = np.stack([_image(rng, h, w, "regions") for _ in range(n)])
     r = ctx.analyze_rgb_batch(rgb, k=6)
-    # one image: [K1 of band 1] + K1 of band 2 + finish; a batch: (K1 + finish) per chunk
-    assert ctx.last_launch_count() == (3 if w * h >= 4 << 20 else 2) if n == 1 else 4
+    # one image: [K1 of band 1] + K1 of band 2, the last K1 finishing the image
+    # itself; a batch: (K1 + finish_kernel) per chunk of several images
+    lc = ctx.last_launch_count()
+    assert lc in ((2, 3) if w * h >= 4 << 20 else (1, 2)) if n == 1 else lc == 4
     r2 = unfused.analyze_rgb_batch(rgb, k=6)
     for i in range(n):
         e = orc.analyze(orc.rgb_to_gray(rgb[i]), 6)
