@@ -35,6 +35,9 @@
  *   kohler_cuda_submit / _collect -> the per-frame loops of src/bench.cpp:264-284 at PCIe
  *                                   speed (two frames in flight; no reference counterpart)
  *   kohler_cuda_set_pipeline_depth -> throughput mode for device loops (no counterpart)
+ *   kohler_cuda_multi_curve / _analyze -> fast_contrast_curve's row-block split
+ *                                   (src/fast.cpp:42-61) over several GPUs + NCCL
+ *   kohler_cuda_multi_analyze_batch -> per-image calls sharded over several GPUs
  *
  * Results are bit-identical to the reference: integer curves exactly, the
  * double curve bit-for-bit (IEEE division of exactly-representable operands),
@@ -245,6 +248,45 @@ int kohler_cuda_segment_batch_device(kohler_cuda_ctx *ctx, const uint8_t *px, in
 int kohler_cuda_segment_batch(kohler_cuda_ctx *ctx, const uint8_t *px, int n, int w, int h,
                               int k, uint8_t *out, int *thresholds, int *ts_counts,
                               int *status);
+
+/* ---- device groups: several GPUs of one box (ABI 1.3) -------------------
+ * One host thread drives the group: one context per device plus one NCCL
+ * communicator per device (ncclCommInitAll; NCCL is loaded at run time, a
+ * group of more than one device fails with KOHLER_CUDA_ERROR without it).
+ * devices == NULL means devices 0 .. ndev-1; a device may not repeat. */
+typedef struct kohler_cuda_multi kohler_cuda_multi;
+int kohler_cuda_multi_create(const int *devices, int ndev, kohler_cuda_multi **out);
+void kohler_cuda_multi_destroy(kohler_cuda_multi *group);
+int kohler_cuda_multi_size(const kohler_cuda_multi *group);
+/* 1 if the group reduces through NCCL (always for ndev > 1). */
+int kohler_cuda_multi_uses_nccl(const kohler_cuda_multi *group);
+
+/* fast_contrast_curve of ONE host image over the group (replaces
+ * kohler::fast_contrast_curve's row-block split, src/fast.cpp:36-62): device
+ * b of B owns rows [h*b/B, h*(b+1)/B) (fast.cpp:42,53-55), uploads them plus
+ * one halo row and computes the exact band partial (as
+ * kohler_cuda_band_curve_device); ONE NCCL all-reduce of the 512 u64
+ * partials merges them like merge_accumulators (src/curve.cpp:16-30).
+ * Synchronous; sum/card: 256 u64 host outputs (either may be NULL). */
+int kohler_cuda_multi_curve(kohler_cuda_multi *group, const uint8_t *px, int w, int h,
+                            size_t pitch, uint64_t *sum, uint64_t *card);
+
+/* The same curve + mean_contrast + optimal_threshold + top_k_local_maxima
+ * (selection on the group's first device); outputs and return value as
+ * kohler_cuda_analyze. */
+int kohler_cuda_multi_analyze(kohler_cuda_multi *group, const uint8_t *px, int w, int h,
+                              size_t pitch, int k, uint64_t *sum, uint64_t *card, double *values,
+                              uint8_t *defined, int *t0, int *topk, int *topk_count);
+
+/* A host batch sharded by image over the group (contiguous shards whose
+ * sizes differ by at most one image; no collective), each shard through
+ * kohler_cuda_analyze_batch on its device, concurrently.  Arguments and
+ * outputs as kohler_cuda_analyze_batch. */
+int kohler_cuda_multi_analyze_batch(kohler_cuda_multi *group, const uint8_t *px, int n, int w,
+                                    int h, size_t pitch, size_t image_stride, int k,
+                                    uint64_t *sums, uint64_t *cards, double *values,
+                                    uint8_t *defined, int *t0s, int *topks, int *topk_counts,
+                                    int *status);
 
 #ifdef __cplusplus
 }

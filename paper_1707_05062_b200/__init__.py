@@ -5,13 +5,13 @@ The product is the CUDA library ``lib/libkohler_cuda.so`` (C ABI in
 (headers under ``include/kohler/``).  This package is the Python host layer
 over the same C ABI.
 """
-from .api import (BatchResult, ContrastCurve, Context, GrayImage, LabelImage, MeanContrastCurve,
+from .api import (BatchResult, ContrastCurve, Context, DeviceGroup, GrayImage, LabelImage, MeanContrastCurve,
                   NoBoundaryError, ThresholdSet, analyze_batch, classify, default_context,
                   direct_contrast_curve, fast_contrast_curve, mean_contrast, merge_accumulators,
                   optimal_threshold, pair_contribution, quantize, top_k_local_maxima)
 
 __all__ = [
-    "BatchResult", "ContrastCurve", "Context", "GrayImage", "LabelImage", "MeanContrastCurve",
+    "BatchResult", "ContrastCurve", "Context", "DeviceGroup", "GrayImage", "LabelImage", "MeanContrastCurve",
     "NoBoundaryError", "ThresholdSet", "analyze_batch", "classify", "default_context",
     "direct_contrast_curve", "fast_contrast_curve", "mean_contrast", "merge_accumulators",
     "optimal_threshold", "pair_contribution", "quantize", "top_k_local_maxima",

@@ -65,6 +65,15 @@ SIGNATURES = {
     "kohler_cuda_segment_batch_device": (
         _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _sz, _sz, _vp, _vp, _vp, _vp]),
     "kohler_cuda_segment_batch": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "kohler_cuda_multi_create": (_i, [_vp, _i, C.POINTER(_vp)]),
+    "kohler_cuda_multi_destroy": (None, [_vp]),
+    "kohler_cuda_multi_size": (_i, [_vp]),
+    "kohler_cuda_multi_uses_nccl": (_i, [_vp]),
+    "kohler_cuda_multi_curve": (_i, [_vp, _vp, _i, _i, _sz, _vp, _vp]),
+    "kohler_cuda_multi_analyze": (
+        _i, [_vp, _vp, _i, _i, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kohler_cuda_multi_analyze_batch": (
+        _i, [_vp, _vp, _i, _i, _i, _sz, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lock = threading.Lock()

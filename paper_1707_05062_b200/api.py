@@ -517,6 +517,73 @@ def direct_contrast_curve(img) -> ContrastCurve:
     return default_context().direct_curve(_as_array(img))
 
 
+class DeviceGroup:
+    """Several GPUs of one box driven from this thread (include/kohler_cuda.h,
+    device groups): one context and one NCCL communicator per device.
+    ``curve``/``analyze`` split ONE image into row bands like the reference's
+    fast_contrast_curve (proj/src/fast.cpp:42-61) and merge the exact band
+    partials with one NCCL all-reduce; ``analyze_batch`` shards a batch by
+    image (no collective)."""
+
+    def __init__(self, devices=None, n: int = 0):
+        lib = _lib.load()
+        devs = list(devices) if devices is not None else list(range(n or 1))
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        _raise_for(lib.kohler_cuda_multi_create(arr, len(devs), C.byref(h)))
+        self._h, self._lib, self.devices = h, lib, devs
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.kohler_cuda_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return int(self._lib.kohler_cuda_multi_size(self._h))
+
+    def uses_nccl(self) -> bool:
+        return bool(self._lib.kohler_cuda_multi_uses_nccl(self._h))
+
+    def curve(self, px: np.ndarray) -> ContrastCurve:
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        h, w = px.shape
+        c = ContrastCurve()
+        _raise_for(self._lib.kohler_cuda_multi_curve(self._h, _ptr(px), w, h, w,
+                                                     _ptr(c.contrast_sum), _ptr(c.cardinality)))
+        return c
+
+    def analyze(self, px: np.ndarray, k: int = 6) -> BatchResult:
+        """One image over the group; a one-image BatchResult (status 1 = no boundary)."""
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        h, w = px.shape
+        r = _alloc_result(1, k, True, True)
+        rc = self._lib.kohler_cuda_multi_analyze(
+            self._h, _ptr(px), w, h, w, int(k), _ptr(r.sums), _ptr(r.cards), _ptr(r.values),
+            _ptr(r.defined), _ptr(r.t0), _ptr(r.topk), _ptr(r.topk_count))
+        if rc not in (_lib.KOHLER_OK, _lib.KOHLER_NO_BOUNDARY):
+            _raise_for(rc)
+        r.status[0] = rc
+        return r
+
+    def analyze_batch(self, px: np.ndarray, k: int = 6) -> BatchResult:
+        px = np.ascontiguousarray(px, dtype=np.uint8)
+        if px.ndim == 2:
+            px = px[None]
+        n, h, w = px.shape
+        r = _alloc_result(n, k, True, True)
+        _raise_for(self._lib.kohler_cuda_multi_analyze_batch(
+            self._h, _ptr(px), n, w, h, w, w * h, int(k), _ptr(r.sums), _ptr(r.cards),
+            _ptr(r.values), _ptr(r.defined), _ptr(r.t0), _ptr(r.topk), _ptr(r.topk_count),
+            _ptr(r.status)))
+        return r
+
+
 def mean_contrast(curve: ContrastCurve) -> MeanContrastCurve:
     return default_context().select_host(curve.contrast_sum, curve.cardinality)
 

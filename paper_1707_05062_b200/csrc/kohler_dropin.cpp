@@ -16,6 +16,14 @@
 // One process-wide context on device $KOHLER_CUDA_DEVICE (default 0) is
 // created on first use; calls are serialised on it, so concurrent callers are
 // safe and get identical results.  No CPU fallback: failures throw.
+//
+// Multi-GPU: with $KOHLER_CUDA_DEVICES set (a comma-separated device list,
+// e.g. "0,1,2,3"), fast_contrast_curve runs over that device group instead:
+// the reference's row-block split over the GPUs (src/fast.cpp:42-61; one band
+// per device instead of one per worker thread) with the band partials merged
+// by one NCCL all-reduce (kohler_cuda_multi_curve).  The result is the same
+// integer curve for any split, exactly as the reference's is for any
+// `workers`.
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -51,6 +59,37 @@ kohler_cuda_ctx* context()
     if (!ctx)
         throw std::runtime_error(error);
     return ctx;
+}
+
+// The device group of $KOHLER_CUDA_DEVICES, or null when it is unset.
+kohler_cuda_multi* group()
+{
+    static std::once_flag once;
+    static kohler_cuda_multi* g = nullptr;
+    static std::string error;
+    std::call_once(once, [] {
+        const char* env = std::getenv("KOHLER_CUDA_DEVICES");
+        if (!env || !*env)
+            return;
+        std::vector<int> devs;
+        for (const char* p = env; *p;) {
+            char* end = nullptr;
+            const long d = std::strtol(p, &end, 10);
+            if (end == p) {
+                error = std::string("kohler: bad KOHLER_CUDA_DEVICES '") + env + "'";
+                return;
+            }
+            devs.push_back((int)d);
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (kohler_cuda_multi_create(devs.data(), (int)devs.size(), &g) != KOHLER_OK) {
+            error = std::string("kohler: device group ") + env + ": " + kohler_cuda_last_error();
+            g = nullptr;
+        }
+    });
+    if (!g && !error.empty())
+        throw std::runtime_error(error);
+    return g;
 }
 
 // Status -> the reference's exception types.
@@ -111,6 +150,12 @@ ContrastCurve fast_contrast_curve(const GrayImage& img, unsigned workers)
     if (workers < 1)
         throw std::invalid_argument("fast_contrast_curve: workers must be at least 1");
     ContrastCurve curve;
+    if (kohler_cuda_multi* g = group()) {
+        raise_for(kohler_cuda_multi_curve(g, img.row(0), img.width(), img.height(),
+                                          static_cast<std::size_t>(img.width()),
+                                          curve.contrast_sum.data(), curve.cardinality.data()));
+        return curve;
+    }
     raise_for(kohler_cuda_curve(context(), img.row(0), img.width(), img.height(),
                                 static_cast<std::size_t>(img.width()),
                                 curve.contrast_sum.data(), curve.cardinality.data()));

@@ -355,7 +355,7 @@ struct kohler_cuda_ctx {
 
 extern "C" {
 
-int kohler_cuda_abi_version(void) { return 101; }
+int kohler_cuda_abi_version(void) { return 103; }
 
 const char* kohler_cuda_last_error(void) { return g_last_error.c_str(); }
 
@@ -1041,3 +1041,5 @@ int kohler_cuda_top_k_local_maxima(kohler_cuda_ctx* ctx, const double* values,
 }
 
 } // extern "C"
+
+#include "kohler_multi.cuh"  // multi-GPU C ABI (device groups, NCCL)

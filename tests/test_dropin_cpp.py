@@ -33,3 +33,19 @@ def test_dropin_cpp_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.startswith("PASS")
+
+
+@pytest.mark.gpu
+def test_dropin_cpp_on_a_device_group(tmp_path):
+    """The same C++ checks with KOHLER_CUDA_DEVICES set: fast_contrast_curve
+    runs through the device-group path (row band per device, NCCL all-reduce
+    of the partials; here a group of the one visible GPU)."""
+    import oracle
+    oracle.build(ref=False)
+    exe = str(tmp_path / "dropin_test")
+    build(exe)
+    env = dict(os.environ, KOHLER_CUDA_DEVICES="0")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    # (NCCL prints its version line at communicator creation)
+    assert r.stdout.strip().splitlines()[-1].startswith("PASS")

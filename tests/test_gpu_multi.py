@@ -1,0 +1,76 @@
+"""The multi-GPU C ABI (kohler_cuda_multi_*, include/kohler_cuda.h "device
+groups"): one host thread, one context + one NCCL communicator per device.
+Only one GPU is visible to the tests, so the group has one member here; the
+row-band split and the merge run through the same code for any size (the
+band partials of every split are checked in test_gpu_parity.py and the
+N > 1 host logic in test_bands_gloo.py).  Results must equal the oracle's
+bit for bit (reference fast.cpp:36-62 for any split)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1707_05062_b200 import DeviceGroup, synth
+from paper_1707_05062_b200._lib import KOHLER_INVALID_ARGUMENT
+
+pytestmark = pytest.mark.gpu
+K = 6
+
+
+@pytest.fixture(scope="module")
+def group():
+    g = DeviceGroup([0])
+    yield g
+    g.close()
+
+
+def test_group_uses_nccl(group):
+    assert group.size() == 1
+    assert group.uses_nccl()  # the all-reduce path runs even for one member
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (16, 1), (129, 7), (512, 512), (5184, 3456)])
+def test_group_curve_and_analyze(group, w, h):
+    orc = oracle.Oracle()
+    if (w, h) == (5184, 3456):
+        x = synth.generate("C2", device="cpu")[0].numpy()
+    else:
+        x = np.random.default_rng(w * 7 + h).integers(0, 256, (h, w), dtype=np.uint8)
+    e = orc.analyze(x, K)
+    c = group.curve(x)
+    assert np.array_equal(c.contrast_sum, e["sum"]) and np.array_equal(c.cardinality, e["card"])
+    r = group.analyze(x, K)
+    assert np.array_equal(r.sums[0], e["sum"]) and np.array_equal(r.cards[0], e["card"])
+    assert np.array_equal(r.values[0].view(np.uint64), np.asarray(e["values"]).view(np.uint64))
+    assert int(r.t0[0]) == e["t0"] and int(r.status[0]) == e["status"]
+    assert r.thresholds(0) == e["topk"]
+
+
+def test_group_no_boundary(group):
+    r = group.analyze(np.full((40, 30), 9, np.uint8), K)
+    assert int(r.status[0]) == 1 and int(r.t0[0]) == -1 and int(r.topk_count[0]) == 0
+    assert not r.cards[0].any()
+
+
+def test_group_batch_shards(group):
+    orc = oracle.Oracle()
+    rng = np.random.default_rng(3)
+    xs = rng.integers(0, 256, (7, 33, 48), dtype=np.uint8)
+    xs[4] = 200  # one boundary-free image inside a shard
+    r = group.analyze_batch(xs, K)
+    for i in range(xs.shape[0]):
+        e = orc.analyze(xs[i], K)
+        assert np.array_equal(r.sums[i], e["sum"]) and np.array_equal(r.cards[i], e["card"])
+        assert int(r.t0[i]) == e["t0"] and int(r.status[i]) == e["status"]
+        assert r.thresholds(i) == e["topk"]
+
+
+def test_group_argument_errors():
+    with pytest.raises(ValueError):
+        DeviceGroup([0, 0])  # a device listed twice
+    with pytest.raises(Exception):
+        DeviceGroup([])
+    g = DeviceGroup([0])
+    with pytest.raises(ValueError):
+        g.analyze(np.zeros((4, 4), np.uint8), 0)  # k < 1
+    g.close()
+    assert KOHLER_INVALID_ARGUMENT == 2
