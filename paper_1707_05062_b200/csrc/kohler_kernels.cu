@@ -346,6 +346,7 @@ struct kohler_cuda_ctx {
     int depth = 1;      // K1 launches in flight (kohler_cuda_set_pipeline_depth)
     bool rgb_fused = true;  // K1 reads RGB itself where the layout allows (env KOHLER_RGB_UNFUSED=1: off)
     bool no_cluster = false;  // env KOHLER_NO_CLUSTER=1: small single images take the ticket path (A/B, tests)
+    int cluster_ok = -1;      // -1 unknown; 1 if an 8-CTA cluster of K1 fits this device (checked once)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };

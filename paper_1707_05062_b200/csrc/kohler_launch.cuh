@@ -253,9 +253,36 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     const bool single = n == 1 && !no_finish;
     // (two W copies: the cluster kernels are instantiated for that layout only)
     p.cluster = (single && G <= kClusterMax && !ctx->no_cluster && !rgb && two_w) ? 1 : 0;
+    if (p.cluster && ctx->cluster_ok < 0) {
+        // can a cluster of kClusterMax K1 CTAs (one SM each, 194 KiB) be
+        // co-scheduled at all on this device / partition?  If not, the ticket
+        // form runs instead (same results).
+        KC_CUDA(cudaFuncSetAttribute(walk_kernel<true, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmWideBytes));
+        cudaLaunchConfig_t oc = {};
+        oc.gridDim = dim3((unsigned)kClusterMax);
+        oc.blockDim = dim3(kWalkThreads);
+        oc.dynamicSmemBytes = kSmWideBytes;
+        cudaLaunchAttribute ca[1];
+        ca[0].id = cudaLaunchAttributeClusterDimension;
+        ca[0].val.clusterDim.x = (unsigned)kClusterMax;
+        ca[0].val.clusterDim.y = 1;
+        ca[0].val.clusterDim.z = 1;
+        oc.attrs = ca;
+        oc.numAttrs = 1;
+        int nclusters = 0;
+        const cudaError_t oe =
+            cudaOccupancyMaxActiveClusters(&nclusters, walk_kernel<true, true, false, true>, &oc);
+        ctx->cluster_ok = (oe == cudaSuccess && nclusters > 0) ? 1 : 0;
+        if (oe != cudaSuccess)
+            (void)cudaGetLastError();  // not sticky; clear it
+    }
+    if (ctx->cluster_ok == 0)
+        p.cluster = 0;
     p.self_finish = (single && !p.cluster && G <= kSelfFinishMax) ? 1 : 0;
     if (p.cluster)
         p.early_trigger = 1;
+
     p.hist_out = hist_out;
     p.sums = o.sums;
     p.cards = o.cards;
