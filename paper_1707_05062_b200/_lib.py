@@ -11,7 +11,10 @@ import os
 import threading
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libkohler_cuda.so")
+# KOHLER_CUDA_LIB selects another build of the same ABI, e.g. the
+# bounds-checked lib/libkohler_cuda_checked.so (tests/test_gpu_checked.py)
+LIB_PATH = os.environ.get("KOHLER_CUDA_LIB") or os.path.join(LIB_DIR, "libkohler_cuda.so")
+CHECKED_LIB_PATH = os.path.join(LIB_DIR, "libkohler_cuda_checked.so")
 DROPIN_PATH = os.path.join(LIB_DIR, "libkohler_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(LIB_DIR), os.pardir, "include", "kohler_cuda.h")
 

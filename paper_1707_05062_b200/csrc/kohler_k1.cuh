@@ -5,6 +5,11 @@
 
 namespace {
 
+#ifdef KOHLER_CHECKED
+using kohler_walk::chk_g;
+using kohler_walk::chk_sm;
+#endif
+
 // K3 + K4, one CTA (256 threads) per image, launched right after K1 with
 // programmatic dependent launch: waits for K1, sums the accumulator copies
 // (resetting them: the workspace is self-cleaning), rebuilds count/sum with
@@ -280,6 +285,10 @@ __device__ __forceinline__ void border_prefetch(const WideParams& p, int img, co
         const int r = i >= nc ? (i >= 2 * nc ? 2 : 1) : 0, ci = i - r * nc;
         const int y = r == 0 ? 0 : ylast + (r - 1);
         const uint8_t* src = base + (size_t)y * p.pitch + 16 * (s.ca + ci);
+        KCHK({
+            chk_sm(dst + r * kBorderRow + 16 * ci, 16);
+            chk_g(src, 16, p.px, p.px + (size_t)(p.n - 1) * p.image_stride + (size_t)p.buf_rows * p.pitch);
+        });
 #ifndef KOHLER_PROBE_NO_BORDER_COPY
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + r * kBorderRow + 16 * ci),
                      "l"(src)
@@ -438,6 +447,10 @@ struct LaneGeo {
     int nrows;         // own rows of the walk (0: no task)
     int e;             // index of the last real pixel of the segment if < 16
     int jlo, jcl;      // ring position j loads row y0 - 1 + clamp(j, jlo, jcl)
+#ifdef KOHLER_CHECKED
+    const uint8_t* g_lo;  // the input buffer (checked builds)
+    const uint8_t* g_hi;
+#endif
 };
 
 template <bool RGB>
@@ -459,6 +472,9 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
         // loads past the buffer's last row re-read it: the down row of the
         // image's last row is the row itself (equal "fake" down pairs)
         L.jcl = p.buf_rows - L.y0;
+#ifdef KOHLER_CHECKED
+        L.jcl += p.inject;  // the negative control: one row past the buffer
+#endif
     } else {
         L.y0 = 1;  // a valid address (row 0), never used
         L.nrows = 0;
@@ -469,6 +485,10 @@ __device__ __forceinline__ LaneGeo lane_geo(const WideParams& p, const uint8_t* 
     L.pd = lane == 0 ? -16 : (int)F::seg;
     L.pds = lane == 0 ? (int)F::lpad : (int)(F::rpad - F::seg * 31);
     L.pad = ((lane == 0) & (L.x0 > 0)) | ((lane == 31) & (L.e > 15)) ? 1u : 0u;
+#ifdef KOHLER_CHECKED
+    L.g_lo = p.px;
+    L.g_hi = p.px + (size_t)(p.n - 1) * p.image_stride + (size_t)p.buf_rows * p.pitch;
+#endif
     return L;
 }
 
@@ -481,6 +501,14 @@ __device__ __forceinline__ void fetch_row(const LaneGeo& L, int j, uint32_t pitc
 {
     // 64-bit row offset (once per segment start: no cost in the walk)
     const uint8_t* src = L.p + (size_t)(uint32_t)min(max(j, L.jlo), L.jcl) * pitch;
+    KCHK({
+        chk_sm(dst, K1Fmt<RGB>::seg);
+        chk_g(src, K1Fmt<RGB>::seg, L.g_lo, L.g_hi);
+        if (L.pad) {
+            chk_sm(dst + L.pds, 16);
+            chk_g(src + L.pd, 16, L.g_lo, L.g_hi);
+        }
+    });
     if constexpr (RGB) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
@@ -512,6 +540,10 @@ struct FetchStream {
     int left;     // positions the pointer may still advance
     uint32_t pl;  // lane 0 with a left neighbour
     uint32_t pr;  // lane 31 with a right neighbour
+#ifdef KOHLER_CHECKED
+    const uint8_t* g_lo;
+    const uint8_t* g_hi;
+#endif
 };
 
 __device__ __forceinline__ FetchStream fetch_stream(const LaneGeo& L, int j, uint32_t pitch,
@@ -523,12 +555,28 @@ __device__ __forceinline__ FetchStream fetch_stream(const LaneGeo& L, int j, uin
     f.left = L.jcl - j;
     f.pl = L.pad && lane == 0;
     f.pr = L.pad && lane == 31;
+#ifdef KOHLER_CHECKED
+    f.g_lo = L.g_lo;
+    f.g_hi = L.g_hi;
+#endif
     return f;
 }
 
 template <bool RGB>
 __device__ __forceinline__ void fetch_next(FetchStream& f, uint32_t pitch, uint32_t dst)
 {
+    KCHK({
+        chk_sm(dst, K1Fmt<RGB>::seg);
+        chk_g(f.src, K1Fmt<RGB>::seg, f.g_lo, f.g_hi);
+        if (f.pl) {
+            chk_sm(dst + (RGB ? 1536u : 512u), 16);
+            chk_g(f.src - 16, 16, f.g_lo, f.g_hi);
+        }
+        if (f.pr) {
+            chk_sm(dst + (RGB ? 64u : 32u), 16);
+            chk_g(f.src + (RGB ? 48 : 16), 16, f.g_lo, f.g_hi);
+        }
+    });
     if constexpr (RGB) {
         // segment = 3 chunks; left pad: slot + lpad <- src - 16 (lane 0 at
         // slot + 0); right pad: slot + rpad = lane 31's segment + 64 <- src + 48
@@ -579,6 +627,11 @@ struct NbrSel {
 template <bool RGB>
 __device__ __forceinline__ void read_row_shfl(kohler_walk::Row& r, uint32_t seg, const NbrSel& n)
 {
+    KCHK({
+        chk_sm(seg, RGB ? 48u : 16u);
+        if (n.pad)
+            chk_sm(seg + n.pad_off, RGB ? 4u : 1u);
+    });
     uint32_t pb = 0;
     if constexpr (RGB) {
         // 48 bytes of interleaved RGB -> 16 luma bytes (the reference's luma601);

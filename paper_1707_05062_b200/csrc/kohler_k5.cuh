@@ -5,6 +5,11 @@
 
 namespace {
 
+#ifdef KOHLER_CHECKED
+using kohler_walk::chk_g;
+using kohler_walk::chk_sm;
+#endif
+
 // ---------------------------------------------------------------------------
 // K5 twalk_kernel: batches of small images with the three-event column walk.
 // The 32 lanes of every warp are split into NG = 32/LG lane groups; group g
@@ -84,6 +89,10 @@ __device__ __forceinline__ LaneGeo tw_geo(const TwParams& p, long long img, int 
     }
     L.p = p.px + (size_t)(act ? img : 0) * p.image_stride + (long long)(L.y0 - 1) * (long long)p.pitch +
           L.x0;
+#ifdef KOHLER_CHECKED
+    L.g_lo = p.px;
+    L.g_hi = p.px + (size_t)(p.n - 1) * p.image_stride + (size_t)p.h * p.pitch;
+#endif
     return L;
 }
 

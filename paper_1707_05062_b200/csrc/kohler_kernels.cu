@@ -74,6 +74,9 @@ struct WideParams {
     int early_trigger;  // pipelined launches: let the next launch start at once (disjoint SMs)
     int self_finish;    // single-image launch: the CTA that flushes last runs K3 + K4 (no finish_kernel)
     int cluster;        // single small image: the grid is one cluster, reduced over DSMEM (no accumulator)
+#ifdef KOHLER_CHECKED
+    int inject;  // negative control of the checked build: read one row past the buffer end
+#endif
     uint32_t* hist_out;  // [n][256] pixel histogram (atomically accumulated), or null
     uint64_t* sums;
     uint64_t* cards;
@@ -347,6 +350,7 @@ struct kohler_cuda_ctx {
     bool rgb_fused = true;  // K1 reads RGB itself where the layout allows (env KOHLER_RGB_UNFUSED=1: off)
     bool no_cluster = false;  // env KOHLER_NO_CLUSTER=1: small single images take the ticket path (A/B, tests)
     int cluster_ok = -1;      // -1 unknown; 1 if an 8-CTA cluster of K1 fits this device (checked once)
+    bool inject = false;      // checked builds, env KOHLER_CHECKED_INJECT=1: deliberate off-by-one (tests)
     bool wide_attr_set = false;
     bool select_attr_set = false;
 };
@@ -385,6 +389,8 @@ int kohler_cuda_create(int device, kohler_cuda_ctx** out)
         ctx->rgb_fused = !(e && e[0] && e[0] != '0');
         const char* c = std::getenv("KOHLER_NO_CLUSTER");
         ctx->no_cluster = c && c[0] && c[0] != '0';
+        const char* inj = std::getenv("KOHLER_CHECKED_INJECT");
+        ctx->inject = inj && inj[0] && inj[0] != '0';
     }
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);

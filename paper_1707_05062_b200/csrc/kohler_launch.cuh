@@ -284,6 +284,9 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         p.early_trigger = 1;
 
     p.hist_out = hist_out;
+#ifdef KOHLER_CHECKED
+    p.inject = ctx->inject ? 1 : 0;
+#endif
     p.sums = o.sums;
     p.cards = o.cards;
     p.values = o.values;

@@ -87,19 +87,74 @@ __device__ __forceinline__ uint32_t qstep(uint32_t nf, uint32_t to_form)
     return __vimin_s16x2_relu(__vadd2(to_form, nf), 0x00020002u);
 }
 
+// ---- checked builds (-DKOHLER_CHECKED, lib/libkohler_cuda_checked.so) ----
+// compute-sanitizer is not available on the GPU pool, so the checked build
+// asserts its own bounds: every shared-memory counter event inside the
+// counter block, every other shared access inside the CTA's dynamic window,
+// every cp.async source inside the input buffer.  A violation prints where
+// and traps (the call then fails with a CUDA error).  Each kernel sets the
+// ranges once per CTA (chk_init) before its first access.
+#ifdef KOHLER_CHECKED
+// The ranges come from the hardware, not from shared state: the dynamic
+// window [cvta(dyn), + %dynamic_smem_size) (carrying the cluster rank bits
+// like every access), counter events at or above kCtrLo inside it; the
+// global source range travels in LaneGeo / FetchStream (g_lo, g_hi).
+constexpr uint32_t kCtrLo = 0x10000;  // lowest counter-block address of any kernel
+__device__ __noinline__ void chk_fail(int code, uint32_t a)
+{
+    printf("KOHLER_CHECKED violation %d at 0x%x (block %d thread %d)\n", code, a, (int)blockIdx.x,
+           (int)threadIdx.x);
+    __trap();
+}
+__device__ __forceinline__ void chk_window(uint32_t& lo, uint32_t& hi)
+{
+    extern __shared__ __align__(16) unsigned char kohler_dyn_smem[];
+    uint32_t sz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sz));
+    lo = (uint32_t)__cvta_generic_to_shared(kohler_dyn_smem);
+    hi = lo + sz;
+}
+__device__ __forceinline__ void chk_sm(uint32_t a, uint32_t bytes)
+{
+    uint32_t lo, hi;
+    chk_window(lo, hi);
+    if (a < lo || a + bytes > hi || (a & (bytes >= 4 ? 3 : 0)))
+        chk_fail(2, a);
+}
+__device__ __forceinline__ void chk_ctr(uint32_t a)
+{
+    chk_sm(a, 4);
+    if ((a & 0x00FFFFFFu) < kCtrLo)
+        chk_fail(1, a);
+}
+__device__ __forceinline__ void chk_g(const void* p, uint32_t bytes, const uint8_t* g_lo,
+                                      const uint8_t* g_hi)
+{
+    const uint8_t* q = static_cast<const uint8_t*>(p);
+    if (q < g_lo || q + bytes > g_hi)
+        chk_fail(3, (uint32_t)(uintptr_t)q);
+}
+#define KCHK(x) x
+#else
+#define KCHK(x) do { } while (0)
+#endif
+
 __device__ __forceinline__ void red_inc(uint32_t saddr)
 {
+    KCHK(chk_ctr(saddr));
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr));
 }
 
 template <uint32_t OFF>
 __device__ __forceinline__ void red_add_imm(uint32_t saddr, uint32_t v)
 {
+    KCHK(chk_ctr(saddr + OFF));
     asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(saddr), "r"(v), "n"(OFF));
 }
 
 __device__ __forceinline__ void red_add(uint32_t saddr, uint32_t v)
 {
+    KCHK(chk_sm(saddr, 4));
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v));
 }
 
