@@ -119,8 +119,11 @@ __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
 
 // Standalone selection for 256-level curves: one warp per curve, 8 curves per
 // CTA, lane L holding thresholds 8L..8L+7 in registers (vector loads), the
-// register-resident selection of kohler_walk.cuh.
-__global__ void __launch_bounds__(256) select256_kernel(const SelectParams p)
+// register-resident selection of kohler_walk.cuh.  The selection is a
+// latency-bound chain of shuffles: 5 CTAs per SM (<= 48 registers, a few
+// spilled to L1) instead of the 3 that 68 registers allowed gave C5 (K5 +
+// this kernel per batch) 1051 -> 1089 Gpx/s.
+__global__ void __launch_bounds__(256, 5) select256_kernel(const SelectParams p)
 {
     __shared__ double smv[8][128];
     __shared__ int smt[8][128];
