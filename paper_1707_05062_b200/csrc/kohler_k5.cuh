@@ -396,11 +396,23 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 tot[(1 * 16 + warp) * NG + gi] = tg;
             }
             __syncthreads();
-            long long cc = 0, cg = 0;
-            for (int w2 = 0; w2 < warp; ++w2) {
-                cc += tot[(0 * 16 + w2) * NG + gi];
-                cg += tot[(1 * 16 + w2) * NG + gi];
-            }
+            // carry of the earlier warps' totals: the image's 4 lanes (q4)
+            // load 4 warps' totals each, independent loads, then two
+            // shuffles (a serial 15-load chain made warp 15 the round's
+            // straggler at the final barrier)
+            auto carry = [&](int kind) -> long long {
+                long long c = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int w2 = 4 * q4 + i;
+                    if (w2 < warp)
+                        c += tot[(kind * 16 + w2) * NG + gi];
+                }
+                c += __shfl_xor_sync(0xFFFFFFFFu, c, 8);
+                c += __shfl_xor_sync(0xFFFFFFFFu, c, 16);
+                return c;
+            };
+            const long long cc = carry(0), cg = carry(1);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 cd[i] += cc;  // card
@@ -410,9 +422,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             if (q4 == 0)
                 tot[(2 * 16 + warp) * NG + gi] = ts;
             __syncthreads();
-            long long cs = 0;
-            for (int w2 = 0; w2 < warp; ++w2)
-                cs += tot[(2 * 16 + w2) * NG + gi];
+            const long long cs = carry(2);
             const long long im = i0 + gi;
             if (im < p.n) {
                 // 64-bit stores straight from the register pairs: STG.128 made
