@@ -539,7 +539,13 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             for (int i = tid; i < NG * (int)(kTwCorrStride / 4); i += kTwThreads)
                 reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
-        __syncthreads();
+        // LG = 4 needs no barrier here: every counter piece was cleared before
+        // the hand-off barrier, and the next round touches the exchange /
+        // carry arrays only after its own barriers, which every warp reaches
+        // after this round's last read of them; a warp done with its stores
+        // starts the next round's walk while the others finish theirs
+        if constexpr (LG != 4)
+            __syncthreads();
         TWCYC(4);
         pos += (uint32_t)P;
         G = N;
