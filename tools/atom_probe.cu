@@ -34,6 +34,52 @@ __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) { asm volatile("
 //  5 as 1, ADD of a register value instead of +1
 //  6 as 1, rows drawn from 256 (one table half), +1
 //  7 as 1, 16 instructions alternate between two tables 64 KiB apart
+// Pattern 8: warps 0-7 run the random-row lane-striped atomics of pattern 1
+// while warps 8-15 stream 16-byte cp.async copies from global memory into a
+// separate shared buffer (like K1/K5's row ring): does ncu's
+// l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom count the
+// arriving copy data as atomic "conflicts"?
+__global__ void __launch_bounds__(512, 1) probe_mixed(uint32_t* out, const uint4* src, int iters)
+{
+    extern __shared__ __align__(16) uint32_t hist[];
+    for (int i = threadIdx.x; i < 32768; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(hist);
+    if (warp < 8) {
+        uint32_t seed = mix(blockIdx.x * 4096 + threadIdx.x * 7 + 1);
+        uint32_t a[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            a[j] = base + (mix(seed + j * 0x9e3779b9u) & 511u) * 128u + lane * 4u;  // rows 0..511
+        for (int it = 0; it < iters; ++it) {
+            const uint32_t x = (uint32_t)(it & 7) << 7;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                red_inc(a[j] ^ x);
+        }
+    } else {
+        // copy ring: 4 slots x 512 B per warp above row 512 (bytes 64 KiB+)
+        const uint32_t ring = base + 65536u + (warp - 8) * 2048u + lane * 16u;
+        const uint4* g = src + (size_t)blockIdx.x * 65536 + (warp - 8) * 32 + lane;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring + j * 512u),
+                             "l"(g + ((it * 4 + j) & 255) * 256)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t s = 0;
+    for (int i = threadIdx.x; i < 16384; i += blockDim.x) s += hist[i];
+    atomicAdd(out, s);
+}
+
 template <int PATTERN>
 __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, int iters)
 {
@@ -118,5 +164,14 @@ int main()
     run<5>("random_rows_add_reg", d, sms);
     run<6>("random_rows_256", d, sms);
     run<7>("random_rows_two_tables", d, sms);
+    {
+        uint4* src;
+        CK(cudaMalloc(&src, (size_t)sms * 65536 * 16));
+        CK(cudaMemset(src, 1, (size_t)sms * 65536 * 16));
+        CK(cudaFuncSetAttribute(probe_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+        probe_mixed<<<sms, 512, 128 * 1024>>>(d, src, 4096);
+        CK(cudaDeviceSynchronize());
+        std::printf("{\"pattern\":\"mixed_atomics_and_cp_async\",\"ran\":1}\n");
+    }
     return 0;
 }
