@@ -124,6 +124,16 @@ __device__ void finish_from_vals(const WideParams& p, int img, unsigned char* sm
         mean[tid] = cc ? (double)cs / (double)cc : 0.0;
         def[tid] = cc ? 1 : 0;
     }
+    __syncthreads();
+    // the selection runs before the wait too, into shared memory (<= 128
+    // maxima exist); only the stores follow the previous launch
+    int* s_ints = reinterpret_cast<int*>(scr + 5248);  // t0, count, status, -, topk[128]
+    if (p.select && tid < 256) {
+        const int st = block_select256(mean, def, p.k, scr, 1, s_ints, s_ints + 4, s_ints + 1);
+        if (tid == 0)
+            s_ints[2] = st;
+    }
+    __syncthreads();
     pdl_wait();
     if (tid < 256) {
         const uint64_t cs = csum[tid], cc = ccard[tid];
@@ -136,13 +146,18 @@ __device__ void finish_from_vals(const WideParams& p, int img, unsigned char* sm
         if (p.defined)
             p.defined[(size_t)img * 256 + tid] = def[tid];
     }
-    __syncthreads();
-    if (p.select && tid < 256) {
-        const int st = block_select256(mean, def, p.k, scr, 1, p.t0s ? p.t0s + img : nullptr,
-                                       p.topks ? p.topks + (size_t)img * p.k : nullptr,
-                                       p.topk_counts ? p.topk_counts + img : nullptr);
-        if (tid == 0 && p.status)
-            p.status[img] = st;
+    if (p.select) {
+        const int cnt = s_ints[1];
+        if (tid == 0) {
+            if (p.t0s)
+                p.t0s[img] = s_ints[0];
+            if (p.topk_counts)
+                p.topk_counts[img] = cnt;
+            if (p.status)
+                p.status[img] = s_ints[2];
+        }
+        if (p.topks && tid < cnt)
+            p.topks[(size_t)img * p.k + tid] = s_ints[4 + tid];
     }
     __syncthreads();
 }
