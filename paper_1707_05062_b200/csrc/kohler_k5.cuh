@@ -48,6 +48,9 @@ constexpr int kTwImgWords = (kTwH + 4 * kTwArr + 3) / 4 * 4;
 // LDS.128 reads of a quarter warp are conflict free (a 1024-byte stride made
 // them 8-way conflicts, ncu r7).
 constexpr uint32_t kTwCorrStride = 1040;
+#ifndef KOHLER_TW_SLOTS
+#define KOHLER_TW_SLOTS 3
+#endif
 
 template <int LG>
 struct TwLayout {
@@ -58,9 +61,13 @@ struct TwLayout {
     // 32 lane segments (512 B, 128-byte aligned), then 2 pads per group
     static constexpr uint32_t kSlot = (512 + 32 * NG + 127) / 128 * 128;
     static constexpr uint32_t kRing = 0;  // + up to 127 B of alignment
-    static constexpr uint32_t kRingBytes = kTwWarps * kRingSlots * kSlot + 128;
-    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][260]
-    static constexpr uint32_t kTot = kCorr + NG * kTwCorrStride;  // i64 [3][16 warps][NG] scan carries
+    // ring slots per warp (KOHLER_TW_SLOTS, default 3: 2 rows in flight; 4
+    // measured 0.4 % slower on C5)
+    static constexpr int kSlots = KOHLER_TW_SLOTS;
+    static constexpr int kAhead = kSlots - 1;
+    static constexpr uint32_t kRingBytes = kTwWarps * kSlots * kSlot + 128;
+    static constexpr uint32_t kCorr = kRingBytes;  // int[NG][260] (not with one W copy)
+    static constexpr uint32_t kTot = kCorr + (kOneW ? 0u : NG * kTwCorrStride);  // i64 [3][16 warps][NG] scan carries
     // LG = 4 flush: boundary values handed from warp w - 1 to warp w
     static constexpr uint32_t kXch = kTot + 3 * 16 * NG * 8;  // uint4 [16 warps][8 images]
     static constexpr uint32_t kXchC = kXch + 16 * 8 * 16;     // int [16 warps][8 images]
@@ -128,7 +135,10 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
     const int task = warp * LG + lig;
     const int P = p.R + 2;
     const uint32_t ring = (smbase + Lay::kRing + 127u) & ~127u;
-    const uint32_t seg0 = ring + (uint32_t)warp * (kRingSlots * Lay::kSlot) + (uint32_t)lane * 16u;
+    constexpr int AH = Lay::kAhead;
+    const uint32_t seg0 = ring + (uint32_t)warp * (Lay::kSlots * Lay::kSlot) + (uint32_t)lane * 16u;
+    const uint32_t slot_end = seg0 + Lay::kSlots * Lay::kSlot;
+    uint32_t sl_cur = seg0, sl_prev = seg0 + (Lay::kSlots - 1) * Lay::kSlot;
     const uint32_t padl = 512u + 32u * g - 16u * lane;  // group pads, relative to the segment
     const uint32_t padr = padl + 16u;
     auto geo = [&](long long i0) {
@@ -141,20 +151,20 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
     const long long stride = (long long)gridDim.x * NG;
     long long i0 = (long long)blockIdx.x * NG;
     LaneGeo G = geo(i0);
-    fetch_row<false>(G, 0, pitch, seg0);
-    fetch_row<false>(G, 1, pitch, seg0 + Lay::kSlot);
-    fetch_row<false>(G, 2, pitch, seg0 + 2 * Lay::kSlot);
+#pragma unroll
+    for (int f = 0; f < AH; ++f)
+        fetch_row<false>(G, f, pitch, seg0 + f * Lay::kSlot);
     {
         uint4* z = reinterpret_cast<uint4*>(hist);
         for (int i = tid; i < (int)(kHistBytes / 16); i += kTwThreads)
             z[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < NG * (int)(kTwCorrStride / 4); i += kTwThreads)
-            reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
+        if constexpr (!Lay::kOneW)
+            for (int i = tid; i < NG * (int)(kTwCorrStride / 4); i += kTwThreads)
+                reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
     }
     __syncthreads();
     bool waited = false;
     Car X, Y;
-    uint32_t pos = 0;
 #ifdef KOHLER_PHASES  // tools/tile_probe.cu: per-CTA cycles of the round phases
     long long tw_t = clock64(), tw_acc[5] = {0, 0, 0, 0, 0};
 #define TWCYC(i) do { const long long t_ = clock64(); tw_acc[i] += t_ - tw_t; tw_t = t_; } while (0)
@@ -178,16 +188,20 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             constexpr int WC = decltype(wc)::value;
             constexpr bool CROSS = decltype(cross)::value;
             constexpr uint32_t kOffW = (WC && !Lay::kOneW) ? kOffW1 : kOffW0;
-            const uint32_t q = pos + (uint32_t)j;
-            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            if (AH > 2)
+                asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
             __syncwarp();
             Row r;  // read first: the prefetch issue covers the LDS latency
-            read_row_shfl<false>(r, seg0 + (q & 3u) * Lay::kSlot, nb);
-            const uint32_t pref = seg0 + ((q + 3u) & 3u) * Lay::kSlot;
-            if (!CROSS || j + 3 < P)
-                fetch_row<false>(G, j + 3, pitch, pref);
+            read_row_shfl<false>(r, sl_cur, nb);
+            const uint32_t pref = sl_prev;  // slot of position j + AH (j - 1's, read already)
+            sl_prev = sl_cur;
+            sl_cur = sl_cur + Lay::kSlot == slot_end ? seg0 : sl_cur + Lay::kSlot;
+            if (!CROSS || j + AH < P)
+                fetch_row<false>(G, j + AH, pitch, pref);
             else if (has_next)
-                fetch_row<false>(N, j + 3 - P, pitch, pref);
+                fetch_row<false>(N, j + AH - P, pitch, pref);
             else
                 asm volatile("cp.async.commit_group;" ::: "memory");
             absorb<ALIGNED>(D, r, lane4, G.e);
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         using W1 = std::integral_constant<int, 1>;
         using NC = std::false_type;
         using CR = std::true_type;
-        if (P > 4) {
+        if (P > AH + 1) {
             step(X, Y, 0, K0{}, W0{}, NC{});
             step(Y, X, 1, K1{}, W1{}, NC{});
         } else {
@@ -264,7 +278,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             step(Y, X, 1, K1{}, W1{}, CR{});
         }
         int j = 2;
-        for (; j + 4 < P; j += 2) {
+        for (; j + AH + 1 < P; j += 2) {
             step(X, Y, j, K2{}, W0{}, NC{});
             step(Y, X, j + 1, K2{}, W1{}, NC{});
         }
@@ -547,7 +561,6 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
         if constexpr (LG != 4)
             __syncthreads();
         TWCYC(4);
-        pos += (uint32_t)P;
         G = N;
     }
 #ifdef KOHLER_PHASES
