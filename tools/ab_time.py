@@ -18,6 +18,7 @@ from paper_1707_05062_b200 import Context, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C2,C3,C4,C5")
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--depth", type=int, default=0, help="0: 3 for C1/C2, else 1")
 a = ap.parse_args()
 ctx = Context(0)
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -33,7 +34,7 @@ for name in a.configs.split(","):
          "t0": torch.zeros(n, dtype=torch.int32, device="cuda"),
          "topk": torch.zeros((n, 6), dtype=torch.int32, device="cuda"),
          "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda")}
-    ctx.set_pipeline_depth(3 if name in ("C1", "C2") else 1)
+    ctx.set_pipeline_depth(a.depth or (3 if name in ("C1", "C2") else 1))
 
     def step(i):
         ctx.analyze_batch_device(bufs[i % copies], w, h, w, w * h, n, 6, o)
