@@ -127,7 +127,7 @@ int band_step(kohler_cuda_multi* g, int b, const uint8_t* px, int w, int h, size
     const int held = std::min(r1 + 1, h) - r0;
     MC(cudaSetDevice(m.device));
     const size_t dp = ((size_t)w + 15) / 16 * 16;
-    if (held > 0) {
+    if (r1 > r0) {  // (more devices than rows: some bands are empty)
         const size_t need = dp * (size_t)held;
         if (need > m.band_cap) {
             if (m.band)
