@@ -253,7 +253,9 @@ int kohler_cuda_segment_batch(kohler_cuda_ctx *ctx, const uint8_t *px, int n, in
  * One host thread drives the group: one context per device plus one NCCL
  * communicator per device (ncclCommInitAll; NCCL is loaded at run time, a
  * group of more than one device fails with KOHLER_CUDA_ERROR without it).
- * devices == NULL means devices 0 .. ndev-1; a device may not repeat. */
+ * devices == NULL means devices 0 .. ndev-1; a device may not repeat
+ * (except with KOHLER_MULTI_VIRTUAL=1 in the environment at creation: a test
+ * mode in which members may share a GPU and the partials merge on the host). */
 typedef struct kohler_cuda_multi kohler_cuda_multi;
 int kohler_cuda_multi_create(const int *devices, int ndev, kohler_cuda_multi **out);
 void kohler_cuda_multi_destroy(kohler_cuda_multi *group);

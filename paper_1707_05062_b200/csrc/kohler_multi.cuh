@@ -76,6 +76,7 @@ struct Member {
 struct kohler_cuda_multi {
     std::vector<Member> m;
     bool use_nccl = false;
+    bool virt = false;  // KOHLER_MULTI_VIRTUAL=1: members may share a device, host merge (tests)
     std::mutex mu;
 };
 
@@ -156,6 +157,25 @@ int band_step(kohler_cuda_multi* g, int b, const uint8_t* px, int w, int h, size
     return KOHLER_OK;
 }
 
+// Without NCCL (a virtual group, or one member): the members' partials summed
+// on the host into the first member's buffer (u64 wraparound sum, exactly
+// merge_accumulators, src/curve.cpp:16-30).
+int merge_without_nccl(kohler_cuda_multi* g)
+{
+    if (g->use_nccl || g->m.size() < 2)
+        return KOHLER_OK;
+    std::vector<uint64_t> acc(512, 0), part(512);
+    for (Member& m : g->m) {
+        MC(cudaSetDevice(m.device));
+        MC(cudaMemcpy(part.data(), m.part, 512 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 512; ++i)
+            acc[i] += part[i];
+    }
+    MC(cudaSetDevice(g->m[0].device));
+    MC(cudaMemcpy(g->m[0].part, acc.data(), 512 * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    return KOHLER_OK;
+}
+
 } // namespace
 
 extern "C" {
@@ -166,10 +186,17 @@ int kohler_cuda_multi_create(const int* devices, int ndev, kohler_cuda_multi** o
         return fail(KOHLER_INVALID_ARGUMENT, "multi: need >= 1 device and an output pointer");
     *out = nullptr;
     auto* g = new kohler_cuda_multi();
+    {
+        // test mode: several members on one GPU (this box has one), merged on
+        // the host instead of by NCCL -- exercises the row-block split,
+        // empty bands and the merge arithmetic of a B-device group
+        const char* v = std::getenv("KOHLER_MULTI_VIRTUAL");
+        g->virt = v && v[0] && v[0] != '0';
+    }
     std::vector<int> devs(ndev);
     for (int i = 0; i < ndev; ++i)
         devs[i] = devices ? devices[i] : i;
-    for (int i = 0; i < ndev; ++i)
+    for (int i = 0; i < ndev && !g->virt; ++i)
         for (int j = 0; j < i; ++j)
             if (devs[i] == devs[j]) {
                 delete g;
@@ -191,7 +218,7 @@ int kohler_cuda_multi_create(const int* devices, int ndev, kohler_cuda_multi** o
         if (e != cudaSuccess)
             rc = fail(KOHLER_CUDA_ERROR, std::string("multi: ") + cudaGetErrorString(e));
     }
-    if (rc == KOHLER_OK) {
+    if (rc == KOHLER_OK && !g->virt) {
         Nccl& n = nccl();
         if (n.ok()) {
             std::vector<ncclComm_t> comms(ndev);
@@ -255,6 +282,8 @@ int kohler_cuda_multi_curve(kohler_cuda_multi* g, const uint8_t* px, int w, int 
     std::lock_guard<std::mutex> lk(g->mu);
     g_last_error.clear();
     int rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
+    if (rc == KOHLER_OK)
+        rc = merge_without_nccl(g);
     if (rc)
         return rc;
     Member& m0 = g->m[0];
@@ -279,6 +308,8 @@ int kohler_cuda_multi_analyze(kohler_cuda_multi* g, const uint8_t* px, int w, in
     std::lock_guard<std::mutex> lk(g->mu);
     g_last_error.clear();
     int rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
+    if (rc == KOHLER_OK)
+        rc = merge_without_nccl(g);
     if (rc)
         return rc;
     // selection on the merged curve, on the first device (K4)

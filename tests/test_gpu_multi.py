@@ -74,3 +74,26 @@ def test_group_argument_errors():
         g.analyze(np.zeros((4, 4), np.uint8), 0)  # k < 1
     g.close()
     assert KOHLER_INVALID_ARGUMENT == 2
+
+
+@pytest.mark.parametrize("members,w,h", [(3, 129, 7), (5, 64, 2), (8, 1, 3), (4, 5184, 3456), (7, 300, 301)])
+def test_virtual_group_row_blocks(members, w, h, monkeypatch):
+    """KOHLER_MULTI_VIRTUAL=1: a group of several members on the one visible
+    GPU (partials merged on the host instead of NCCL).  Exercises the
+    row-block split of a B-device group -- uneven blocks, more members than
+    rows (empty bands), the halo rows -- against the oracle."""
+    monkeypatch.setenv("KOHLER_MULTI_VIRTUAL", "1")
+    g = DeviceGroup([0] * members)
+    assert g.size() == members and not g.uses_nccl()
+    orc = oracle.Oracle()
+    if (w, h) == (5184, 3456):
+        x = synth.generate("C2", device="cpu")[0].numpy()
+    else:
+        x = np.random.default_rng(members * 1000 + w + h).integers(0, 256, (h, w), dtype=np.uint8)
+    e = orc.analyze(x, K)
+    c = g.curve(x)
+    assert np.array_equal(c.contrast_sum, e["sum"]) and np.array_equal(c.cardinality, e["card"])
+    r = g.analyze(x, K)
+    assert int(r.t0[0]) == e["t0"] and r.thresholds(0) == e["topk"]
+    assert np.array_equal(r.values[0].view(np.uint64), np.asarray(e["values"]).view(np.uint64))
+    g.close()
