@@ -10,15 +10,19 @@
 //                        the CTA flush turns the counters into 512 exact
 //                        integer combinations, REDG.ADD.64 into the image's
 //                        accumulators.
-//   K3/K4 finish_kernel: PDL-chained after K1, one CTA per image: sums and
-//                        resets the accumulators, int64 prefix scans (count,
-//                        sum), IEEE f64 mean curve, optimal threshold, top-k.
+//   K3/K4 finish      : PDL-chained finish_kernel after K1, one CTA per image:
+//                        sums and resets the accumulators, int64 prefix scans
+//                        (count, sum), IEEE f64 mean curve, optimal threshold,
+//                        top-k.  Single images with small grids finish inside
+//                        K1 instead: one thread-block cluster reduced over DSMEM
+//                        (<= 8 CTAs) or the last-flushing CTA (ticket, <= 24).
 //   K5  twalk_kernel   : batches of small images (lane groups own images;
 //                        curves rebuilt in the CTA), + select256_kernel (K4).
 //   select_kernel / select256_kernel : selection on given curves.
 //   direct_kernel      : definition-level curve (direct.cpp restated).
 //   hist_kernel / map_kernel : segmentation (classify / quantize).
 //   luma_kernel        : Rec. 601 colour ingest.
+// kohler_multi.cuh (included at the end) holds the multi-GPU device groups.
 #include <cuda_runtime.h>
 
 #include <algorithm>
