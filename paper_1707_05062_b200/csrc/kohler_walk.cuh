@@ -59,6 +59,17 @@ constexpr int kMaxEventsPerWord = 8191;
 constexpr uint32_t kTo = 0x02020202u;              // unpack fill: lanes b + 512 ("to" form)
 constexpr uint32_t kNeutral = 0x00010001u;         // q of an equal pair, both lanes
 
+// Constants ptxas must not see through: the integer ALU pipe
+// (PRMT / IADD3 / LOP3 / LEA / VIADDMNMX) is the saturated math pipe of the
+// walk and the FMA pipe (IMAD) is half idle, but ptxas strength-reduces every
+// multiply by a KNOWN power of two or by -1 back into an ALU instruction
+// (LEA, LEA.HI, IADD3).  A __constant__ word is a run-time value to the
+// compiler, so x * c + y stays an IMAD with a constant-bank operand.
+#ifndef KOHLER_FMA_SHIFT
+#define KOHLER_FMA_SHIFT 4
+#endif
+__constant__ uint32_t kOpaque[4] = {1u << 24, 0xFFFFFFFFu, 65536u, 0u};
+
 struct Row {  // one prefetched 16-pixel row segment + its neighbour bytes
     uint32_t w[4];
     uint32_t ln, rn;
@@ -79,7 +90,11 @@ struct Car {  // a row segment in the form the accumulation uses
 // the high half of the constant pre-pays.  to + nf = to - from + 1.
 __device__ __forceinline__ uint32_t qfrom(uint32_t to_form)
 {
+#if KOHLER_FMA_SHIFT & 2
+    return to_form * kOpaque[1] + 0x00020001u;
+#else
     return 0x00020001u - to_form;
+#endif
 }
 
 __device__ __forceinline__ uint32_t qstep(uint32_t nf, uint32_t to_form)
@@ -187,9 +202,18 @@ __device__ __forceinline__ void absorb(Car& Y, const Row& r0, uint32_t lane4, in
     for (int j = 0; j < 4; ++j) {
         Y.e[j] = __byte_perm(r.w[j], kTo, 0x4240);
         Y.o[j] = __byte_perm(r.w[j], kTo, 0x4341);
+#if KOHLER_FMA_SHIFT & 1
+        // the high 16-bit lanes (pixels 4j+2, 4j+3) on the FMA pipe:
+        // e >> 8 = (b2 + 512) << 8 | (b0 + 512) >> 8 = (b2 << 8) + 0x20002
+        Y.A[4 * j + 0] = __byte_perm(r.w[j], lane4, 0x7604);
+        Y.A[4 * j + 1] = __byte_perm(r.w[j], lane4, 0x7614);
+        Y.A[4 * j + 2] = __umulhi(Y.e[j], kOpaque[0]) + (lane4 - 0x20002u);
+        Y.A[4 * j + 3] = __umulhi(Y.o[j], kOpaque[0]) + (lane4 - 0x20002u);
+#else
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             Y.A[4 * j + k] = __byte_perm(r.w[j], lane4, 0x7604 | (k << 4));
+#endif
     }
     Y.ln = r.ln;
     Y.rn = r.rn;
@@ -236,7 +260,11 @@ __device__ __forceinline__ void b_terms(const Car& X, const uint32_t (&qre)[4],
 __device__ __forceinline__ uint32_t inc_of(uint32_t lanes, int hi)
 {
     if (!hi)
+#if KOHLER_FMA_SHIFT & 4
+        return lanes * kOpaque[2] + 1u;
+#else
         return lanes * 65536u + 1u;
+#endif
     uint32_t r;
     asm("lop3.b32 %0, %1, 0xFFFF0000, %2, 0xEA;" : "=r"(r) : "r"(lanes), "r"(1u));  // (a & b) | c
     return r;
