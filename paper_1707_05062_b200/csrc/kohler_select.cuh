@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
 // this kernel per batch) 1051 -> 1089 Gpx/s.
 __global__ void __launch_bounds__(256, 5) select256_kernel(const SelectParams p)
 {
-    __shared__ double smv[8][128];
+    __shared__ unsigned long long smv[8][128];
     __shared__ int smt[8][128];
     // the next launch may start at once: every kernel that reads this one's
     // outputs executes griddepcontrol.wait before it does

@@ -288,84 +288,61 @@ __device__ __forceinline__ uint32_t b_of(const uint32_t (&Be)[4], const uint32_t
 //                               above both neighbouring runs (one-sided at the
 //                               ends), rank by (value desc, t asc), keep k,
 //                               report ascending.
-// Cross-lane information moves by warp scans of per-lane summaries:
-//   prefix: the last defined value left of a lane;
-//   suffix: the value of the leftmost run right of a lane and the value of
-//           the run after it (a run may continue across lanes).
+// Cross-lane information moves by warp votes and indexed shuffles (see
+// warp_select256_regs).
 namespace kohler_walk {
 
-struct RunSum {      // summary of a range of thresholds (its defined entries)
-    int has;         // any defined entry
-    double lv;       // leftmost run value
-    int lnext_has;   // a second run exists
-    double lnext;    // value of the run after the leftmost run
-};
 
-__device__ __forceinline__ RunSum runsum_combine(const RunSum& A, const RunSum& B)
+// Order-preserving 64-bit key of a finite double (-0.0 counts as +0.0, like
+// the IEEE comparison): a > b  <=>  key(a) > key(b),  a == b  <=>  equal keys.
+// Every finite value has a key > 0, so 0 stands for "no value".
+__device__ __forceinline__ unsigned long long order_key(double x)
 {
-    // A left of B
-    if (!A.has)
-        return B;
-    if (!B.has)
-        return A;
-    RunSum r;
-    r.has = 1;
-    r.lv = A.lv;
-    if (A.lnext_has) {
-        r.lnext_has = 1;
-        r.lnext = A.lnext;
-    } else if (A.lv == B.lv) {  // A is one run continuing into B's leftmost run
-        r.lnext_has = B.lnext_has;
-        r.lnext = B.lnext;
-    } else {
-        r.lnext_has = 1;
-        r.lnext = B.lv;
-    }
-    return r;
+    const long long b = __double_as_longlong(x + 0.0);
+    return b < 0 ? ~(unsigned long long)b : (unsigned long long)b | 0x8000000000000000ull;
 }
 
-__device__ __forceinline__ RunSum runsum_shfl_down(const RunSum& x, int off)
+__device__ __forceinline__ double shfl_f64(double x, int src)
 {
-    RunSum y;
-    y.has = __shfl_down_sync(0xFFFFFFFFu, x.has, off);
-    y.lv = __shfl_down_sync(0xFFFFFFFFu, x.lv, off);
-    y.lnext_has = __shfl_down_sync(0xFFFFFFFFu, x.lnext_has, off);
-    y.lnext = __shfl_down_sync(0xFFFFFFFFu, x.lnext, off);
-    return y;
+    return __shfl_sync(0xFFFFFFFFu, x, src);
 }
 
-// better (value desc, t asc) of two candidates; t < 0 = none
-__device__ __forceinline__ void best_of(double& bv, int& bt, double ov, int ot)
+// v/d: this lane's 8 values / defined flags (t = 8 lane + j).  mk/mt: smem
+// scratch for the maxima (>= 128 entries: keys and thresholds).  Returns 1
+// (no boundary) or 0.
+//
+// The rules only compare each defined value with the previous defined one,
+// so a lane reduces its 8 entries to three bit masks -- S: a run starts here
+// (first defined value, or it differs from the previous one), U: it is a
+// rise (or nothing precedes it), F: it is a fall -- in straight-line
+// predicated code, and a run start is a local maximum iff it is a rise and
+// the NEXT run start, wherever it is, is a fall or does not exist.  Across
+// lanes that takes one indexed shuffle (the last defined value left of the
+// lane) and votes (which lanes hold a run start, and whether their first one
+// is a fall); the earlier forms moved whole run summaries by log-step scans
+// (~165 dependent SHFL and ~1180 instructions per curve; now 2 SHFL, ~12
+// votes / REDUX).  Then:
+//   compaction prefix sums of the per-lane maxima counts by votes per bit;
+//   top-k      rank of every local maximum among all of them (value desc,
+//              t asc) from the shared-memory list, keep rank < k;
+//   optimum    the rank-0 maximum (the first threshold of the first run with
+//              the largest value is always a local maximum), by REDUX.
+__device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int k,
+                                   unsigned long long* mk, int* mt, int* out_t0, int* out_topk,
+                                   int* out_count)
 {
-    if (ot >= 0 && (bt < 0 || ov > bv || (ov == bv && ot < bt))) {
-        bv = ov;
-        bt = ot;
-    }
-}
-
-// v/d: this lane's 8 values / defined flags (t = 8 lane + j).  mv/mt: smem
-// scratch for the maxima (>= 128 entries).  Returns 1 (no boundary) or 0.
-__device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int k, double* mv,
-                                   int* mt, int* out_t0, int* out_topk, int* out_count)
-{
+    constexpr unsigned kFull = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    // optimal threshold
-    double bv = 0.0;
-    int bt = -1;
+    unsigned dm = 0;
+    double lastv = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (d[j] && (bt < 0 || v[j] > bv)) {
-            bv = v[j];
-            bt = 8 * lane + j;
-        }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, off);
-        const int ot = __shfl_xor_sync(0xFFFFFFFFu, bt, off);
-        best_of(bv, bt, ov, ot);
+    for (int j = 0; j < 8; ++j) {
+        dm |= (d[j] ? 1u : 0u) << j;
+        lastv = d[j] ? v[j] : lastv;
     }
-    if (bt < 0) {  // nothing defined: NoBoundaryError
+    const unsigned H = __ballot_sync(kFull, dm != 0);
+    if (H == 0) {  // nothing defined: NoBoundaryError
         if (lane == 0) {
             if (out_t0)
                 *out_t0 = -1;
@@ -374,121 +351,82 @@ __device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int
         }
         return 1;
     }
-    // prefix: last defined value strictly left of this lane
-    int ph = 0;
-    double pv = 0.0;
+    // the last defined value strictly left of this lane
+    const unsigned Hl = H & lt;
+    double pv = shfl_f64(lastv, Hl ? 31 - __clz(Hl) : lane);
+    bool ph = Hl != 0;
+    // every defined entry against the previous defined value
+    unsigned S = 0, U = 0, F = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (d[j]) {
-            ph = 1;
-            pv = v[j];
-        }
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int oh = __shfl_up_sync(0xFFFFFFFFu, ph, off);
-        const double ov = __shfl_up_sync(0xFFFFFFFFu, pv, off);
-        if (lane >= off && !ph) {
-            ph = oh;
-            pv = ov;
-        }
+    for (int j = 0; j < 8; ++j) {
+        const bool gt = v[j] > pv, ne = v[j] != pv;
+        const bool st = d[j] && (!ph || ne);
+        const bool up = d[j] && (!ph || gt);
+        const bool fl = d[j] && ph && ne && !gt;
+        S |= (st ? 1u : 0u) << j;
+        U |= (up ? 1u : 0u) << j;
+        F |= (fl ? 1u : 0u) << j;
+        pv = d[j] ? v[j] : pv;
+        ph = ph || d[j];
     }
-    int cin_h = __shfl_up_sync(0xFFFFFFFFu, ph, 1);
-    double cin_v = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
-    if (lane == 0)
-        cin_h = 0;
-    // suffix: run summary of everything right of this lane
-    RunSum mine{0, 0.0, 0, 0.0};
+    // the first run start right of this lane: none, or a fall => a maximum may end here
+    const unsigned BS = __ballot_sync(kFull, S != 0);
+    const unsigned BF = __ballot_sync(kFull, (F & (S & (0u - S))) != 0);
+    const unsigned BSr = BS & (0xFFFFFFFEu << lane);
+    unsigned carry = BSr ? (BF >> (__ffs(BSr) - 1)) & 1u : 1u;
+    unsigned ok = 0;
 #pragma unroll
     for (int j = 7; j >= 0; --j) {
-        if (d[j]) {
-            RunSum e{1, v[j], 0, 0.0};
-            mine = runsum_combine(e, mine);
-        }
+        const unsigned m = (S >> j) & 1u;
+        ok |= (carry & m) << j;
+        carry = m ? (F >> j) & 1u : carry;
     }
-    RunSum suf = mine;  // inclusive suffix over lanes >= lane
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const RunSum o = runsum_shfl_down(suf, off);
-        if (lane + off < 32)
-            suf = runsum_combine(suf, o);
-    }
-    RunSum right = runsum_shfl_down(suf, 1);  // lanes > lane
-    if (lane == 31)
-        right.has = 0;
-    // per entry, right to left: value of the next run after the entry's run
-    // (nr_has/nr), tracking the run the entry belongs to (cur)
-    bool is_start[8];
-    double nxt[8];
-    bool nxt_has[8];
-    {
-        int ch = right.has;
-        double cv = right.lv;                 // value of the run right of here
-        int nh = right.lnext_has;
-        double nv = right.lnext;              // and the run after it
-#pragma unroll
-        for (int j = 7; j >= 0; --j) {
-            if (d[j]) {
-                if (!ch) {
-                    ch = 1;
-                    cv = v[j];
-                    nh = 0;
-                } else if (v[j] != cv) {
-                    nh = 1;
-                    nv = cv;
-                    cv = v[j];
-                }
-                nxt_has[j] = nh;
-                nxt[j] = nv;
-            } else {
-                nxt_has[j] = false;
-                nxt[j] = 0.0;
-            }
-        }
-    }
-    // left to right: run starts and their maxima
-    unsigned maxmask = 0;
-    {
-        int hh = cin_h;
-        double hv = cin_v;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            is_start[j] = false;
-            if (d[j]) {
-                is_start[j] = !hh || v[j] != hv;
-                if (is_start[j] && (!hh || hv < v[j]) && (!nxt_has[j] || nxt[j] < v[j]))
-                    maxmask |= 1u << j;
-                hh = 1;
-                hv = v[j];
-            }
-        }
-    }
-    // compact the maxima in t order
+    const unsigned maxmask = S & U & ok;
+    // compact the maxima in t order (a lane has <= 4: strict maxima are never adjacent)
     const int myn = __popc(maxmask);
-    int pre = myn;
+    int pos = 0, nm = 0;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int o = __shfl_up_sync(0xFFFFFFFFu, pre, off);
-        if (lane >= off)
-            pre += o;
+    for (int b = 0; b < 3; ++b) {
+        const unsigned m = __ballot_sync(kFull, (myn >> b) & 1);
+        pos += __popc(m & lt) << b;
+        nm += __popc(m) << b;
     }
-    const int nm = __shfl_sync(0xFFFFFFFFu, pre, 31);
-    int pos = pre - myn;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
         if (maxmask & (1u << j)) {
-            mv[pos] = v[j];
+            mk[pos] = order_key(v[j]);
             mt[pos] = 8 * lane + j;
             ++pos;
         }
     __syncwarp();
-    // top-k: k rounds of warp argmax over the maxima (<= 128: 4 per lane)
-    double cv[4];
+    // candidates lane + 32 q (t order)
+    unsigned long long ck[4];
     int ct[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int i = lane + 32 * q;
-        ct[q] = i < nm ? mt[i] : -1;
-        cv[q] = i < nm ? mv[i] : 0.0;
+        const bool in = i < nm;
+        ck[q] = in ? mk[i] : 0ull;
+        ct[q] = in ? mt[i] : -1;
+    }
+    // optimal threshold = the largest maximum, ties to the smallest t
+    {
+        unsigned long long key = ck[0];
+        int bt = ct[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+            if (ck[q] > key) {  // later candidates have larger t: strict
+                key = ck[q];
+                bt = ct[q];
+            }
+        const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+        const unsigned mh = __reduce_max_sync(kFull, khi);
+        const bool c1 = khi == mh;
+        const unsigned ml = __reduce_max_sync(kFull, c1 ? klo : 0u);
+        const bool c2 = c1 && klo == ml && bt >= 0;
+        const unsigned t0 = __reduce_min_sync(kFull, c2 ? (unsigned)bt : 0x7FFFFFFFu);
+        if (lane == 0 && out_t0)
+            *out_t0 = (int)t0;
     }
     unsigned sel = 0;  // bit q: candidate lane + 32 q selected
     if (k >= nm) {
@@ -497,43 +435,40 @@ __device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int
             if (ct[q] >= 0)
                 sel |= 1u << q;
     } else {
-        for (int r = 0; r < k; ++r) {
-            double lv = 0.0;
-            int ltt = -1;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (!(sel & (1u << q)))
-                    best_of(lv, ltt, cv[q], ct[q]);
-            double gv = lv;
-            int gt = ltt;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ov = __shfl_xor_sync(0xFFFFFFFFu, gv, off);
-                const int ot = __shfl_xor_sync(0xFFFFFFFFu, gt, off);
-                best_of(gv, gt, ov, ot);
+        // rank among all maxima (value desc, t asc = list index asc)
+        int rank[4] = {0, 0, 0, 0};
+        if (nm <= 32) {
+#pragma unroll 4
+            for (int j = 0; j < nm; ++j) {
+                const unsigned long long x = mk[j];  // broadcast
+                rank[0] += (x > ck[0] || (x == ck[0] && j < lane)) ? 1 : 0;
             }
+        } else {
+#pragma unroll 2
+            for (int j = 0; j < nm; ++j) {
+                const unsigned long long x = mk[j];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (ct[q] == gt)
-                    sel |= 1u << q;
+                for (int q = 0; q < 4; ++q)
+                    rank[q] += (x > ck[q] || (x == ck[q] && j < lane + 32 * q)) ? 1 : 0;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (ct[q] >= 0 && rank[q] < k)
+                sel |= 1u << q;
     }
     // report ascending t: candidates are in t order (index lane + 32 q)
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const bool s = (sel >> q) & 1u;
-        const unsigned b = __ballot_sync(0xFFFFFFFFu, s);
+        const unsigned b = __ballot_sync(kFull, s);
         if (s && out_topk)
             out_topk[cnt + __popc(b & lt)] = ct[q];
         cnt += __popc(b);
     }
-    if (lane == 0) {
-        if (out_t0)
-            *out_t0 = bt;
-        if (out_count)
-            *out_count = cnt;
-    }
+    if (lane == 0 && out_count)
+        *out_count = cnt;
     return 0;
 }
 
