@@ -357,6 +357,7 @@ struct kohler_cuda_ctx {
     bool inject = false;      // checked builds, env KOHLER_CHECKED_INJECT=1: deliberate off-by-one (tests)
     bool wide_attr_set = false;
     bool select_attr_set = false;
+    bool select256_attr_set = false;
 };
 
 #include "kohler_launch.cuh"

@@ -396,7 +396,17 @@ int launch_select(kohler_cuda_ctx* ctx, const SelectParams& sp, cudaStream_t str
     if (sp.n_curves == 0)
         return KOHLER_OK;
     if (sp.levels == 256) {
-        KC_CUDA(launch_pdl(select256_kernel, (unsigned)((sp.n_curves + 7) / 8), 256, 0, stream, sp));
+        // persistent: every warp strides over the curves (kohler_select.cuh)
+        if (!ctx->select256_attr_set) {
+            KC_CUDA(cudaFuncSetAttribute(select256_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSel256Smem));
+            KC_CUDA(cudaFuncSetAttribute(select256_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared));
+            ctx->select256_attr_set = true;
+        }
+        const long long ctas = std::min<long long>((sp.n_curves + kSel256Warps - 1) / kSel256Warps,
+                                                   (long long)ctx->sm_count * kSel256CtasPerSm);
+        KC_CUDA(launch_pdl(select256_kernel, (unsigned)ctas, 32 * kSel256Warps, kSel256Smem, stream, sp));
         ctx->last_launches += 1;
         return KOHLER_OK;
     }

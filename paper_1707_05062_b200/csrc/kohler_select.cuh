@@ -117,71 +117,123 @@ __global__ void __launch_bounds__(32) select_kernel(const SelectParams p)
         p.status[cidx] = st;
 }
 
-// Standalone selection for 256-level curves: one warp per curve, 8 curves per
-// CTA, lane L holding thresholds 8L..8L+7 in registers (vector loads), the
-// register-resident selection of kohler_walk.cuh.  The selection is a
-// latency-bound chain of shuffles: 5 CTAs per SM (<= 48 registers, a few
-// spilled to L1) instead of the 3 that 68 registers allowed gave C5 (K5 +
-// this kernel per batch) 1051 -> 1089 Gpx/s.
-__global__ void __launch_bounds__(256, 5) select256_kernel(const SelectParams p)
+// Standalone selection for 256-level curves: one warp per curve, lane L
+// holding thresholds 8L..8L+7 in registers, the register-resident selection
+// of kohler_walk.cuh.  Persistent: 4 CTAs of 10 warps per SM, every warp
+// strides over the curves and, for (sum, card) input, keeps the NEXT curve's
+// 4 KiB in flight (cp.async into its own shared buffer, issued right after
+// the current curve moved from the buffer into registers), so no warp waits
+// on HBM between curves: on C5 the one-curve-per-warp form spent 7 of 12
+// warp-cycles per issue on the loads' scoreboard at 3.0 TB/s
+// (profiles/r02h).  Buffer layout: 16-byte chunk g of [sums | cards] at slot
+// g ^ ((g >> 3) & 3), which makes the lanes' LDS.128 of chunks 4L + q
+// conflict free.
+constexpr int kSel256Warps = 10;   // 55 KiB of shared memory per CTA, 4 CTAs = 40 warps per SM
+constexpr int kSel256CtasPerSm = 4;
+constexpr uint32_t kSel256Buf = 4096;  // per warp: sums[256] | cards[256]
+constexpr uint32_t kSel256PerWarp = kSel256Buf + 128 * 8 + 128 * 4;
+constexpr uint32_t kSel256Smem = kSel256Warps * kSel256PerWarp;
+
+__device__ __forceinline__ uint32_t sel256_slot(uint32_t g)
 {
-    __shared__ unsigned long long smv[8][128];
-    __shared__ int smt[8][128];
+    return ((g & 127u) ^ ((g >> 3) & 3u)) | (g & 128u);  // sums: chunks 0..127, cards: 128..255
+}
+
+__global__ void __launch_bounds__(32 * kSel256Warps, kSel256CtasPerSm)
+select256_kernel(const SelectParams p)
+{
+    // dynamic (kSel256Smem > 48 KiB): per warp the curve buffer, then the maxima keys and thresholds
+    extern __shared__ __align__(16) unsigned char sel_sm[];
+    unsigned char* const wsm = sel_sm + (threadIdx.x >> 5) * kSel256PerWarp;
+    unsigned char* const sbuf_w = wsm;
+    unsigned long long* const smv_w = reinterpret_cast<unsigned long long*>(wsm + kSel256Buf);
+    int* const smt_w = reinterpret_cast<int*>(wsm + kSel256Buf + 128 * 8);
     // the next launch may start at once: every kernel that reads this one's
     // outputs executes griddepcontrol.wait before it does
     pdl_trigger();
     pdl_wait();  // curves may come from the preceding (PDL-overlapped) launch
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const long long cidx = (long long)blockIdx.x * 8 + wq;
-    if (cidx >= p.n_curves)
-        return;
-    const size_t off = (size_t)cidx * 256 + 8 * lane;
-    double v[8];
-    bool d[8];
-    if (p.sums) {
-        uint64_t s[8], c[8];
+    const long long stride = (long long)gridDim.x * kSel256Warps;
+    long long cidx = (long long)blockIdx.x * kSel256Warps + wq;
+    const uint32_t buf = (uint32_t)__cvta_generic_to_shared(sbuf_w);
+    const bool staged = p.sums != nullptr;
+    // copy curve c's sums and cards (2 x 128 chunks of 16 bytes) into the buffer
+    auto prefetch = [&](long long c) {
+        if (c < p.n_curves) {
+            const unsigned char* gs = reinterpret_cast<const unsigned char*>(p.sums + (size_t)c * 256);
+            const unsigned char* gc = reinterpret_cast<const unsigned char*>(p.cards + (size_t)c * 256);
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-            const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(p.sums + off + j);
-            const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(p.cards + off + j);
-            s[j] = a.x;
-            s[j + 1] = a.y;
-            c[j] = b.x;
-            c[j + 1] = b.y;
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t g = (uint32_t)lane + 32u * i;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(buf + 16u * sel256_slot(g)),
+                             "l"(gs + 16u * g)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(buf + 16u * sel256_slot(g + 128u)),
+                             "l"(gc + 16u * g)
+                             : "memory");
+            }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (staged)
+        prefetch(cidx);
+    for (; cidx < p.n_curves; cidx += stride) {
+        const size_t off = (size_t)cidx * 256 + 8 * lane;
+        double v[8];
+        bool d[8];
+        if (staged) {
+            uint64_t s[8], c[8];
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            d[j] = c[j] != 0;
-            v[j] = d[j] ? (double)s[j] / (double)c[j] : 0.0;
-        }
-    } else {
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(
+                    sbuf_w + 16u * sel256_slot(4u * lane + q));
+                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(
+                    sbuf_w + 16u * sel256_slot(4u * lane + q + 128u));
+                s[2 * q] = a.x;
+                s[2 * q + 1] = a.y;
+                c[2 * q] = b.x;
+                c[2 * q + 1] = b.y;
+            }
+            __syncwarp();  // every lane has read the buffer: refill it
+            prefetch(cidx + stride);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            v[j] = p.in_values[off + j];
-            d[j] = p.in_defined[off + j] != 0;
+            for (int j = 0; j < 8; ++j) {
+                d[j] = c[j] != 0;
+                v[j] = d[j] ? (double)s[j] / (double)c[j] : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                v[j] = p.in_values[off + j];
+                d[j] = p.in_defined[off + j] != 0;
+            }
         }
+        if (p.values) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2)
+                *reinterpret_cast<double2*>(p.values + off + j) = make_double2(v[j], v[j + 1]);
+        }
+        if (p.defined) {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                lo |= (d[j] ? 1u : 0u) << (8 * j);
+                hi |= (d[j + 4] ? 1u : 0u) << (8 * j);
+            }
+            *reinterpret_cast<uint2*>(p.defined + off) = make_uint2(lo, hi);
+        }
+        if (!p.want_select)
+            continue;
+        const int st = kohler_walk::warp_select256_regs(
+            v, d, p.k, smv_w, smt_w, p.t0s ? p.t0s + cidx : nullptr,
+            p.topks ? p.topks + (size_t)cidx * p.k : nullptr, p.topk_counts ? p.topk_counts + cidx : nullptr);
+        if (lane == 0 && p.status)
+            p.status[cidx] = st;
+        __syncwarp();  // the maxima scratch is reused by the next curve
     }
-    if (p.values) {
-#pragma unroll
-        for (int j = 0; j < 8; j += 2)
-            *reinterpret_cast<double2*>(p.values + off + j) = make_double2(v[j], v[j + 1]);
-    }
-    if (p.defined) {
-        uint32_t lo = 0, hi = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            lo |= (d[j] ? 1u : 0u) << (8 * j);
-            hi |= (d[j + 4] ? 1u : 0u) << (8 * j);
-        }
-        *reinterpret_cast<uint2*>(p.defined + off) = make_uint2(lo, hi);
-    }
-    if (!p.want_select)
-        return;
-    const int st = kohler_walk::warp_select256_regs(
-        v, d, p.k, smv[wq], smt[wq], p.t0s ? p.t0s + cidx : nullptr,
-        p.topks ? p.topks + (size_t)cidx * p.k : nullptr, p.topk_counts ? p.topk_counts + cidx : nullptr);
-    if (lane == 0 && p.status)
-        p.status[cidx] = st;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 } // namespace
