@@ -260,8 +260,16 @@ typedef struct kohler_cuda_multi kohler_cuda_multi;
 int kohler_cuda_multi_create(const int *devices, int ndev, kohler_cuda_multi **out);
 void kohler_cuda_multi_destroy(kohler_cuda_multi *group);
 int kohler_cuda_multi_size(const kohler_cuda_multi *group);
-/* 1 if the group reduces through NCCL (always for ndev > 1). */
+/* 1 if the group reduces through NCCL (groups of one device, and groups
+ * whose devices cannot map the first device's memory). */
 int kohler_cuda_multi_uses_nccl(const kohler_cuda_multi *group);
+/* 1 if the group runs in peer mode (ABI 1.4): every device's band kernel adds
+ * its exact partial straight into one accumulator on the first device
+ * (system-scope 64-bit reductions over NVLink / NVSwitch peer memory) and the
+ * first device finishes -- no collective.  The default for ndev > 1 when
+ * cudaDeviceCanAccessPeer holds for every member; KOHLER_MULTI_NO_PEER=1 in
+ * the environment at creation keeps the NCCL all-reduce. */
+int kohler_cuda_multi_uses_peer(const kohler_cuda_multi *group);
 
 /* fast_contrast_curve of ONE host image over the group (replaces
  * kohler::fast_contrast_curve's row-block split, src/fast.cpp:36-62): device

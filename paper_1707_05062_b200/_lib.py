@@ -72,6 +72,7 @@ SIGNATURES = {
     "kohler_cuda_multi_destroy": (None, [_vp]),
     "kohler_cuda_multi_size": (_i, [_vp]),
     "kohler_cuda_multi_uses_nccl": (_i, [_vp]),
+    "kohler_cuda_multi_uses_peer": (_i, [_vp]),
     "kohler_cuda_multi_curve": (_i, [_vp, _vp, _i, _i, _sz, _vp, _vp]),
     "kohler_cuda_multi_analyze": (
         _i, [_vp, _vp, _i, _i, _sz, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -521,9 +521,11 @@ class DeviceGroup:
     """Several GPUs of one box driven from this thread (include/kohler_cuda.h,
     device groups): one context and one NCCL communicator per device.
     ``curve``/``analyze`` split ONE image into row bands like the reference's
-    fast_contrast_curve (proj/src/fast.cpp:42-61) and merge the exact band
-    partials with one NCCL all-reduce; ``analyze_batch`` shards a batch by
-    image (no collective)."""
+    fast_contrast_curve (proj/src/fast.cpp:42-61); the band kernels add their
+    exact partials into one accumulator on the first device over peer memory
+    (``uses_peer``), or, where the devices cannot map each other's memory, one
+    NCCL all-reduce merges them; ``analyze_batch`` shards a batch by image (no
+    collective)."""
 
     def __init__(self, devices=None, n: int = 0):
         lib = _lib.load()
@@ -549,6 +551,11 @@ class DeviceGroup:
 
     def uses_nccl(self) -> bool:
         return bool(self._lib.kohler_cuda_multi_uses_nccl(self._h))
+
+    def uses_peer(self) -> bool:
+        """Peer mode: the members' band kernels add straight into one
+        accumulator on the first device (no collective)."""
+        return bool(self._lib.kohler_cuda_multi_uses_peer(self._h))
 
     def curve(self, px: np.ndarray) -> ContrastCurve:
         px = np.ascontiguousarray(px, dtype=np.uint8)

@@ -424,7 +424,11 @@ __device__ void flush_image(const WideParams& p, int img, unsigned char* sm, uns
             reinterpret_cast<long long*>(sm + kSmVal)[t] = val;
         } else if (val != 0) {
             const int copy = blockIdx.x % p.copies;
-            atomicAdd(p.acc + ((size_t)img * p.copies + copy) * 512 + t, (unsigned long long)val);
+            unsigned long long* dst = p.acc + ((size_t)img * p.copies + copy) * 512 + t;
+            if (p.acc_sys)  // the group's shared accumulator on the first GPU, over NVLink
+                atomicAdd_system(dst, (unsigned long long)val);
+            else
+                atomicAdd(dst, (unsigned long long)val);
         }
         if (p.hist_out && t < 256) {
             const uint32_t hv = (uint32_t)hist(t);  // the W words' pixel counts

@@ -78,6 +78,7 @@ struct WideParams {
     int early_trigger;  // pipelined launches: let the next launch start at once (disjoint SMs)
     int self_finish;    // single-image launch: the CTA that flushes last runs K3 + K4 (no finish_kernel)
     int cluster;        // single small image: the grid is one cluster, reduced over DSMEM (no accumulator)
+    int acc_sys;        // acc is another GPU's memory (device groups, peer mode): system-scope REDs
 #ifdef KOHLER_CHECKED
     int inject;  // negative control of the checked build: read one row past the buffer end
 #endif
@@ -365,7 +366,7 @@ struct kohler_cuda_ctx {
 
 extern "C" {
 
-int kohler_cuda_abi_version(void) { return 103; }
+int kohler_cuda_abi_version(void) { return 104; }
 
 const char* kohler_cuda_last_error(void) { return g_last_error.c_str(); }
 

@@ -142,8 +142,12 @@ constexpr long long kSelfFinishMax = 24;
 int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_rows,
                 int h_total, int r0, size_t pitch, size_t image_stride, int k, int select,
                 const BatchOut& o, cudaStream_t stream, int no_finish = 0,
-                uint32_t* hist_out = nullptr, bool rgb = false)
+                uint32_t* hist_out = nullptr, bool rgb = false,
+                unsigned long long* acc_ext = nullptr)
 {
+    // acc_ext (device groups, peer mode; one image, no_finish): the flush adds
+    // into this accumulator -- [kAccCopiesSingle][512] on the group's first
+    // GPU, reached over NVLink -- instead of the context's own
     if (n == 0)
         return KOHLER_OK;
     // rgb: px is interleaved RGB (3 bytes per pixel) and K1 computes the
@@ -232,7 +236,8 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         two_w = !kSingleW || range > e1;
         p.epoch = two_w ? (int)std::max(1.0, std::floor(cap2 / (0.5 + 1.5 / (double)R))) : (int)e1;
     }
-    p.acc = static_cast<unsigned long long*>(ctx->acc.p);
+    p.acc = acc_ext ? acc_ext : static_cast<unsigned long long*>(ctx->acc.p);
+    p.acc_sys = acc_ext ? 1 : 0;
     p.early_trigger = depth > 1 ? 1 : 0;
     p.copies = copies;
     p.tickets = static_cast<unsigned*>(ctx->tickets.p);

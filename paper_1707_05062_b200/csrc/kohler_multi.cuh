@@ -10,11 +10,20 @@
 //       (kohler_cuda_band_curve_device), ONE NCCL all-reduce of the 512 u64
 //       partials merges them like merge_accumulators (src/curve.cpp:16-30),
 //       device 0 runs the selection (K4).
+//       PEER MODE (the default whenever every device of the group can map
+//       the first device's memory, cudaDeviceCanAccessPeer): no collective
+//       and no per-device K3 at all -- every device's K1 flush adds its 512
+//       exact int64 combinations straight into ONE accumulator on the first
+//       device (system-scope RED.ADD.64 over NVLink / NVSwitch, launch_wide's
+//       acc_ext), the first device waits for the members' events and runs a
+//       single finish_kernel (K3 + K4).  Compute and merge are one kernel per
+//       device; KOHLER_MULTI_NO_PEER=1 keeps the NCCL form.
 //   kohler_cuda_multi_analyze_batch : a batch sharded by image (contiguous
 //       shards, sizes differing by at most one), no collective.
 //
-// Part of the translation unit kohler_kernels.cu (included at its end); uses
-// only the public C ABI, the CUDA runtime and fail().  NCCL is loaded at run
+// Part of the translation unit kohler_kernels.cu (included at its end); the
+// NCCL form uses only the public C ABI, peer mode also launch_wide /
+// finish_kernel directly.  NCCL is loaded at run
 // time (dlopen "libnccl.so.2": the copy a host process such as torch already
 // loaded, else the system one), so the library itself has no link-time NCCL
 // dependency; a group of more than one device without NCCL is refused.
@@ -64,6 +73,7 @@ struct Member {
     uint8_t* band = nullptr;  // own rows + halo, 16-byte pitch
     size_t band_cap = 0;
     uint64_t* part = nullptr;  // [sum 256 | card 256] partial, then the merged curve
+    cudaEvent_t ev = nullptr;  // peer mode: this member's band kernel has flushed
     // selection outputs on the first member
     double* values = nullptr;
     uint8_t* defined = nullptr;
@@ -76,7 +86,8 @@ struct Member {
 struct kohler_cuda_multi {
     std::vector<Member> m;
     bool use_nccl = false;
-    bool virt = false;  // KOHLER_MULTI_VIRTUAL=1: members may share a device, host merge (tests)
+    bool virt = false;  // KOHLER_MULTI_VIRTUAL=1: members may share a device (tests)
+    bool peer = false;  // members flush into the first member's accumulator (no collective)
     std::mutex mu;
 };
 
@@ -157,6 +168,108 @@ int band_step(kohler_cuda_multi* g, int b, const uint8_t* px, int w, int h, size
     return KOHLER_OK;
 }
 
+// ---- peer mode ------------------------------------------------------------
+// The group's accumulator: the first member's own K1 accumulator block
+// ([kAccCopiesSingle][512] u64, zero between calls: finish_kernel resets it).
+int peer_acc(kohler_cuda_multi* g, unsigned long long** acc)
+{
+    Member& m0 = g->m[0];
+    MC(cudaSetDevice(m0.device));
+    std::lock_guard<std::mutex> lk(m0.ctx->mu);
+    if (int rc = m0.ctx->acc.ensure((size_t)kAccCopiesSingle * 512 * sizeof(unsigned long long), true))
+        return rc;
+    *acc = static_cast<unsigned long long*>(m0.ctx->acc.p);
+    return KOHLER_OK;
+}
+
+// Member b: upload its rows (+ halo), K1 over the band with the flush aimed
+// at the group's accumulator, record the member's event.  No finish, no sync.
+int peer_band_step(kohler_cuda_multi* g, int b, const uint8_t* px, int w, int h, size_t pitch,
+                   unsigned long long* acc)
+{
+    Member& m = g->m[b];
+    const int B = (int)g->m.size();
+    const int r0 = (int)((long long)h * b / B), r1 = (int)((long long)h * (b + 1) / B);
+    const int held = std::min(r1 + 1, h) - r0;
+    MC(cudaSetDevice(m.device));
+    if (r1 > r0) {  // (more devices than rows: an empty band adds nothing)
+        const size_t dp = ((size_t)w + 15) / 16 * 16;
+        const size_t need = dp * (size_t)held;
+        if (need > m.band_cap) {
+            if (m.band)
+                cudaFree(m.band);
+            m.band = nullptr;
+            m.band_cap = 0;
+            MC(cudaMalloc(&m.band, need));
+            m.band_cap = need;
+        }
+        MC(cudaMemcpy2DAsync(m.band, dp, px + (size_t)r0 * pitch, pitch, (size_t)w, (size_t)held,
+                             cudaMemcpyHostToDevice, m.stream));
+        if (int rc = check_image(1, w, h, dp))
+            return rc;
+        std::lock_guard<std::mutex> lk(m.ctx->mu);
+        m.ctx->last_launches = 0;
+        const BatchOut none{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (int rc = launch_wide(m.ctx, m.band, 1, w, r1 - r0, h, r0, dp, 0, 1, 0, none, m.stream,
+                                 /*no_finish=*/1, nullptr, false, acc))
+            return rc;
+    }
+    MC(cudaEventRecord(m.ev, m.stream));
+    return KOHLER_OK;
+}
+
+// All members' flushes -> one finish_kernel on the first device (K3, and K4
+// if select): sums / cards into m0.part, the selection outputs as given.
+int peer_finish(kohler_cuda_multi* g, unsigned long long* acc, int k, int select, double* values,
+                uint8_t* defined, int* t0, int* topk, int* topk_count, int* status)
+{
+    Member& m0 = g->m[0];
+    MC(cudaSetDevice(m0.device));
+    for (Member& m : g->m)
+        MC(cudaStreamWaitEvent(m0.stream, m.ev, 0));
+    FinishParams fp{};
+    fp.acc = acc;
+    fp.copies = kAccCopiesSingle;
+    fp.k = k;
+    fp.select = select;
+    fp.sums = m0.part;
+    fp.cards = m0.part + 256;
+    fp.values = values;
+    fp.defined = defined;
+    fp.t0s = t0;
+    fp.topks = topk;
+    fp.topk_counts = topk_count;
+    fp.status = status;
+    MC(launch_pdl(finish_kernel, 1u, 256, 0, m0.stream, fp));
+    MC(cudaStreamSynchronize(m0.stream));
+    return KOHLER_OK;
+}
+
+// The band steps of one image in peer mode; on failure the accumulator is
+// cleared again (a later call must start from zero).
+int peer_image(kohler_cuda_multi* g, const uint8_t* px, int w, int h, size_t pitch, int k, int select,
+               double* values, uint8_t* defined, int* t0, int* topk, int* topk_count, int* status)
+{
+    unsigned long long* acc = nullptr;
+    if (int rc = peer_acc(g, &acc))
+        return rc;
+    int rc = for_members(g, [&](int b) { return peer_band_step(g, b, px, w, h, pitch, acc); });
+    if (rc == KOHLER_OK)
+        rc = peer_finish(g, acc, k, select, values, defined, t0, topk, topk_count, status);
+    if (rc != KOHLER_OK) {
+        const std::string keep = g_last_error;
+        for (Member& m : g->m) {
+            cudaSetDevice(m.device);
+            cudaStreamSynchronize(m.stream);
+        }
+        cudaSetDevice(g->m[0].device);
+        cudaMemset(acc, 0, (size_t)kAccCopiesSingle * 512 * sizeof(unsigned long long));
+        (void)cudaGetLastError();
+        g_last_error = keep;
+    }
+    return rc;
+}
+
 // Without NCCL (a virtual group, or one member): the members' partials summed
 // on the host into the first member's buffer (u64 wraparound sum, exactly
 // merge_accumulators, src/curve.cpp:16-30).
@@ -214,11 +327,39 @@ int kohler_cuda_multi_create(const int* devices, int ndev, kohler_cuda_multi** o
         if (e == cudaSuccess)
             e = cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking);
         if (e == cudaSuccess)
+            e = cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming);
+        if (e == cudaSuccess)
             e = cudaMalloc(&m.part, 512 * sizeof(uint64_t));
         if (e != cudaSuccess)
             rc = fail(KOHLER_CUDA_ERROR, std::string("multi: ") + cudaGetErrorString(e));
     }
-    if (rc == KOHLER_OK && !g->virt) {
+    if (rc == KOHLER_OK && ndev > 1) {
+        // peer mode: every member must be able to map the first device's memory
+        const char* np = std::getenv("KOHLER_MULTI_NO_PEER");
+        bool peer = !(np && np[0] && np[0] != '0');
+        for (int i = 1; i < ndev && peer; ++i) {
+            if (devs[i] == devs[0])
+                continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, devs[i], devs[0]) != cudaSuccess || !can) {
+                peer = false;
+                break;
+            }
+            cudaError_t e = cudaSetDevice(devs[i]);
+            if (e == cudaSuccess)
+                e = cudaDeviceEnablePeerAccess(devs[0], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                (void)cudaGetLastError();
+                e = cudaSuccess;
+            }
+            if (e != cudaSuccess) {
+                (void)cudaGetLastError();
+                peer = false;
+            }
+        }
+        g->peer = peer;
+    }
+    if (rc == KOHLER_OK && !g->virt && !g->peer) {
         Nccl& n = nccl();
         if (n.ok()) {
             std::vector<ncclComm_t> comms(ndev);
@@ -260,6 +401,8 @@ void kohler_cuda_multi_destroy(kohler_cuda_multi* g)
         cudaFree(m.values);
         cudaFree(m.defined);
         cudaFree(m.ints);
+        if (m.ev)
+            cudaEventDestroy(m.ev);
         if (m.stream)
             cudaStreamDestroy(m.stream);
         if (m.ctx)
@@ -272,6 +415,8 @@ int kohler_cuda_multi_size(const kohler_cuda_multi* g) { return g ? (int)g->m.si
 
 int kohler_cuda_multi_uses_nccl(const kohler_cuda_multi* g) { return g && g->use_nccl ? 1 : 0; }
 
+int kohler_cuda_multi_uses_peer(const kohler_cuda_multi* g) { return g && g->peer ? 1 : 0; }
+
 int kohler_cuda_multi_curve(kohler_cuda_multi* g, const uint8_t* px, int w, int h, size_t pitch,
                             uint64_t* sum, uint64_t* card)
 {
@@ -281,9 +426,14 @@ int kohler_cuda_multi_curve(kohler_cuda_multi* g, const uint8_t* px, int w, int 
         return rc;
     std::lock_guard<std::mutex> lk(g->mu);
     g_last_error.clear();
-    int rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
-    if (rc == KOHLER_OK)
-        rc = merge_without_nccl(g);
+    int rc;
+    if (g->peer) {
+        rc = peer_image(g, px, w, h, pitch, 1, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    } else {
+        rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
+        if (rc == KOHLER_OK)
+            rc = merge_without_nccl(g);
+    }
     if (rc)
         return rc;
     Member& m0 = g->m[0];
@@ -307,12 +457,6 @@ int kohler_cuda_multi_analyze(kohler_cuda_multi* g, const uint8_t* px, int w, in
         return rc;
     std::lock_guard<std::mutex> lk(g->mu);
     g_last_error.clear();
-    int rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
-    if (rc == KOHLER_OK)
-        rc = merge_without_nccl(g);
-    if (rc)
-        return rc;
-    // selection on the merged curve, on the first device (K4)
     Member& m0 = g->m[0];
     MC(cudaSetDevice(m0.device));
     const int kk = std::min(k, KOHLER_LEVELS);  // more maxima than levels cannot exist
@@ -326,12 +470,29 @@ int kohler_cuda_multi_analyze(kohler_cuda_multi* g, const uint8_t* px, int w, in
         MC(cudaMalloc(&m0.ints, (3 + kk) * sizeof(int)));
         m0.ints_cap = 3 + kk;
     }
-    rc = kohler_cuda_select_device(m0.ctx, m0.part, m0.part + 256, 1, 256, kk, m0.values,
-                                   m0.defined, m0.ints, m0.ints + 3, m0.ints + 1, m0.ints + 2,
-                                   m0.stream);
-    if (rc)
-        return rc;
-    MC(cudaStreamSynchronize(m0.stream));
+    int rc;
+    if (g->peer) {
+        // K3 + K4 in the one finish_kernel behind the members' flushes
+        rc = peer_image(g, px, w, h, pitch, kk, 1, m0.values, m0.defined, m0.ints, m0.ints + 3,
+                        m0.ints + 1, m0.ints + 2);
+        if (rc)
+            return rc;
+    } else {
+        rc = for_members(g, [&](int b) { return band_step(g, b, px, w, h, pitch); });
+        if (rc == KOHLER_OK)
+            rc = merge_without_nccl(g);
+        if (rc)
+            return rc;
+        // selection on the merged curve, on the first device (K4)
+        MC(cudaSetDevice(m0.device));
+        rc = kohler_cuda_select_device(m0.ctx, m0.part, m0.part + 256, 1, 256, kk, m0.values,
+                                       m0.defined, m0.ints, m0.ints + 3, m0.ints + 1, m0.ints + 2,
+                                       m0.stream);
+        if (rc)
+            return rc;
+        MC(cudaStreamSynchronize(m0.stream));
+    }
+    MC(cudaSetDevice(m0.device));
     std::vector<int> hi(3 + kk);
     MC(cudaMemcpy(hi.data(), m0.ints, (3 + kk) * sizeof(int), cudaMemcpyDeviceToHost));
     if (sum)

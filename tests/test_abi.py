@@ -31,7 +31,7 @@ def test_every_declared_symbol_is_exported_and_bound():
         assert hasattr(lib, s), s
         assert s in _lib.SIGNATURES, f"{s} missing from the ctypes binding"
     assert set(_lib.SIGNATURES) == set(syms)
-    assert lib.kohler_cuda_abi_version() == 103
+    assert lib.kohler_cuda_abi_version() == 104
 
 
 def test_dropin_exports_reference_api():

@@ -26,6 +26,7 @@ def group():
 def test_group_uses_nccl(group):
     assert group.size() == 1
     assert group.uses_nccl()  # the all-reduce path runs even for one member
+    assert not group.uses_peer()
 
 
 @pytest.mark.parametrize("w,h", [(1, 1), (16, 1), (129, 7), (512, 512), (5184, 3456)])
@@ -76,24 +77,56 @@ def test_group_argument_errors():
     assert KOHLER_INVALID_ARGUMENT == 2
 
 
+@pytest.mark.parametrize("peer", [True, False])
 @pytest.mark.parametrize("members,w,h", [(3, 129, 7), (5, 64, 2), (8, 1, 3), (4, 5184, 3456), (7, 300, 301)])
-def test_virtual_group_row_blocks(members, w, h, monkeypatch):
+def test_virtual_group_row_blocks(members, w, h, peer, monkeypatch):
     """KOHLER_MULTI_VIRTUAL=1: a group of several members on the one visible
-    GPU (partials merged on the host instead of NCCL).  Exercises the
-    row-block split of a B-device group -- uneven blocks, more members than
-    rows (empty bands), the halo rows -- against the oracle."""
+    GPU.  Exercises the row-block split of a B-device group -- uneven blocks,
+    more members than rows (empty bands), the halo rows -- against the oracle,
+    in both merge forms: peer mode (every member's band kernel adds straight
+    into the first member's accumulator, system-scope REDs, one finish_kernel
+    behind the members' events; the members' kernels run concurrently on
+    their own streams) and, with KOHLER_MULTI_NO_PEER=1, per-member partial
+    curves merged on the host (the stand-in for the NCCL all-reduce)."""
     monkeypatch.setenv("KOHLER_MULTI_VIRTUAL", "1")
+    if not peer:
+        monkeypatch.setenv("KOHLER_MULTI_NO_PEER", "1")
     g = DeviceGroup([0] * members)
-    assert g.size() == members and not g.uses_nccl()
+    assert g.size() == members and not g.uses_nccl() and g.uses_peer() == peer
     orc = oracle.Oracle()
     if (w, h) == (5184, 3456):
         x = synth.generate("C2", device="cpu")[0].numpy()
     else:
         x = np.random.default_rng(members * 1000 + w + h).integers(0, 256, (h, w), dtype=np.uint8)
     e = orc.analyze(x, K)
+    for _ in range(2):  # twice: the shared accumulator must be clean again after a call
+        c = g.curve(x)
+        assert np.array_equal(c.contrast_sum, e["sum"]) and np.array_equal(c.cardinality, e["card"])
+        r = g.analyze(x, K)
+        assert np.array_equal(r.sums[0], e["sum"]) and np.array_equal(r.cards[0], e["card"])
+        assert int(r.t0[0]) == e["t0"] and r.thresholds(0) == e["topk"]
+        assert np.array_equal(r.values[0].view(np.uint64), np.asarray(e["values"]).view(np.uint64))
+    g.close()
+
+
+def test_virtual_peer_group_mixed_calls(monkeypatch):
+    """Peer mode across different images and a boundary-free one: the one
+    accumulator is reused call after call."""
+    monkeypatch.setenv("KOHLER_MULTI_VIRTUAL", "1")
+    g = DeviceGroup([0] * 4)
+    assert g.uses_peer()
+    orc = oracle.Oracle()
+    rng = np.random.default_rng(77)
+    for w, h in [(640, 480), (33, 5), (2000, 37), (16, 16)]:
+        x = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        e = orc.analyze(x, K)
+        r = g.analyze(x, K)
+        assert np.array_equal(r.sums[0], e["sum"]) and np.array_equal(r.cards[0], e["card"])
+        assert int(r.t0[0]) == e["t0"] and r.thresholds(0) == e["topk"]
+    r = g.analyze(np.full((40, 30), 9, np.uint8), K)
+    assert int(r.status[0]) == 1 and int(r.t0[0]) == -1 and not r.cards[0].any()
+    x = rng.integers(0, 256, (100, 100), dtype=np.uint8)
+    e = orc.analyze(x, K)
     c = g.curve(x)
     assert np.array_equal(c.contrast_sum, e["sum"]) and np.array_equal(c.cardinality, e["card"])
-    r = g.analyze(x, K)
-    assert int(r.t0[0]) == e["t0"] and r.thresholds(0) == e["topk"]
-    assert np.array_equal(r.values[0].view(np.uint64), np.asarray(e["values"]).view(np.uint64))
     g.close()

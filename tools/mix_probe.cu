@@ -7,6 +7,9 @@
 //   mode 1: per-lane 16-byte cp.async (LDGSTS.BYPASS), as K1 ships
 //   mode 2: one 512-byte cp.async.bulk (TMA) per warp, mbarrier completion
 //   mode 3: per-lane LDG.128 straight into registers (no ring)
+//   mode 4: K5's pattern with cp.async: 8 lane groups x 64 B from 8 different images
+//           (16 KiB apart) + one 16-byte pad copy per group (8 lanes)
+//   mode 5: K5's pattern with one 80-byte cp.async.bulk per group (8 per warp row)
 // Output: cycles per iteration per SM (16 warps), i.e. the floor of a K1 step
 // if nothing but the memory side mattered.
 //
@@ -28,7 +31,7 @@ __device__ __forceinline__ void red_inc(uint32_t a) { asm volatile("red.shared.a
 
 constexpr int kWarps = 16;
 constexpr uint32_t kHist = 128 * 1024;          // counter block
-constexpr uint32_t kRing = kWarps * 4 * 512;    // 4 slots x 512 B per warp
+constexpr uint32_t kRing = kWarps * 4 * 640;    // 4 slots x 640 B per warp
 constexpr uint32_t kBars = kWarps * 4 * 8;
 
 template <int MODE, bool SHFL>
@@ -40,9 +43,9 @@ __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, const uint4* src,
     for (int i = threadIdx.x; i < (int)(kHist / 4); i += blockDim.x) hist[i] = 0;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t ring = base + kHist + warp * 2048u;
+    const uint32_t ring = base + kHist + warp * 2560u;
     const uint32_t bars = base + kHist + kRing + warp * 32u;
-    if (MODE == 2 && lane == 0) {
+    if ((MODE == 2 || MODE == 5) && lane == 0) {
         for (int s = 0; s < 4; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8u * s));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -62,11 +65,37 @@ __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, const uint4* src,
     const uint4* g = src + ((size_t)(blockIdx.x * kWarps + warp) * rows_per_warp) * 32;
     auto fetch = [&](int it) {
         const uint4* row = g + (size_t)(it & 511) * 32;
-        const uint32_t slot = ring + (uint32_t)(it & 3) * 512u;
+        const uint32_t slot = ring + (uint32_t)(it & 3) * 640u;
         if (MODE == 1) {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot + lane * 16u), "l"(row + lane)
                          : "memory");
             asm volatile("cp.async.commit_group;" ::: "memory");
+        } else if (MODE == 4) {
+            // group g = lane / 4 reads image g (16 KiB apart), 64 B per row; pads by lig == 3
+            const unsigned char* img = reinterpret_cast<const unsigned char*>(g) + (size_t)(lane >> 2) * 16384 +
+                                       (size_t)(it & 127) * 128;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot + lane * 16u),
+                         "l"(img + (lane & 3) * 16)
+                         : "memory");
+            if ((lane & 3) == 3)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot + 512u + (lane >> 2) * 16u),
+                             "l"(img + 64)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        } else if (MODE == 5) {
+            const uint32_t bar = bars + 8u * (it & 3);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 640;" ::"r"(bar) : "memory");
+            __syncwarp();
+            if ((lane & 3) == 0) {
+                const unsigned char* img = reinterpret_cast<const unsigned char*>(g) + (size_t)(lane >> 2) * 16384 +
+                                           (size_t)(it & 127) * 128;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 80, [%2];" ::"r"(
+                        slot + (lane >> 2) * 80u),
+                    "l"(img), "r"(bar)
+                    : "memory");
+            }
         } else if (MODE == 2) {
             if (lane == 0) {
                 const uint32_t bar = bars + 8u * (it & 3);
@@ -92,11 +121,11 @@ __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, const uint4* src,
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
         uint4 r = make_uint4(0, 0, 0, 0);
-        const uint32_t slot = ring + (uint32_t)(it & 3) * 512u + lane * 16u;
-        if (MODE == 1) {
+        const uint32_t slot = ring + (uint32_t)(it & 3) * 640u + (MODE == 5 ? (lane >> 2) * 80u + (lane & 3) * 16u : lane * 16u);
+        if (MODE == 1 || MODE == 4) {
             asm volatile("cp.async.wait_group 2;" ::: "memory");
             __syncwarp();
-        } else if (MODE == 2) {
+        } else if (MODE == 2 || MODE == 5) {
             const uint32_t bar = bars + 8u * (it & 3);
             const uint32_t parity = (uint32_t)(it >> 2) & 1u;
             asm volatile(
@@ -107,7 +136,7 @@ __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, const uint4* src,
                 : "memory");
             __syncwarp();
         }
-        if (MODE == 1 || MODE == 2) {
+        if (MODE == 1 || MODE == 2 || MODE == 4 || MODE == 5) {
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                          : "r"(slot)
@@ -137,9 +166,9 @@ __global__ void __launch_bounds__(512, 1) probe(uint32_t* out, const uint4* src,
             red_inc(c[j] ^ x);
     }
     const long long t1 = clock64();
-    if (MODE == 1)
+    if (MODE == 1 || MODE == 4)
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (MODE == 2) {
+    if (MODE == 2 || MODE == 5) {
         // drain the three copies still in flight
         for (int it = iters; it < iters + 3; ++it) {
             const uint32_t bar = bars + 8u * (it & 3);
@@ -212,5 +241,7 @@ int main()
     run<1, true>("cp_async_16B", d, src, rows_per_warp, sms, dcyc);
     run<2, true>("bulk_512B", d, src, rows_per_warp, sms, dcyc);
     run<3, true>("ldg_128", d, src, rows_per_warp, sms, dcyc);
+    run<4, true>("k5_cp_async_8x64B_plus_pads", d, src, rows_per_warp, sms, dcyc);
+    run<5, true>("k5_bulk_8x80B", d, src, rows_per_warp, sms, dcyc);
     return 0;
 }
