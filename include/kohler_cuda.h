@@ -249,13 +249,16 @@ int kohler_cuda_segment_batch(kohler_cuda_ctx *ctx, const uint8_t *px, int n, in
                               int k, uint8_t *out, int *thresholds, int *ts_counts,
                               int *status);
 
-/* ---- device groups: several GPUs of one box (ABI 1.3) -------------------
- * One host thread drives the group: one context per device plus one NCCL
- * communicator per device (ncclCommInitAll; NCCL is loaded at run time, a
- * group of more than one device fails with KOHLER_CUDA_ERROR without it).
+/* ---- device groups: several GPUs of one box (ABI 1.3; peer mode 1.4) -----
+ * One host thread drives the group: one context per device.  The members'
+ * band partials of one image merge either in peer mode (see
+ * kohler_cuda_multi_uses_peer) or through one NCCL communicator per device
+ * (ncclCommInitAll; NCCL is loaded at run time, a group of more than one
+ * device that can use neither fails with KOHLER_CUDA_ERROR).
  * devices == NULL means devices 0 .. ndev-1; a device may not repeat
  * (except with KOHLER_MULTI_VIRTUAL=1 in the environment at creation: a test
- * mode in which members may share a GPU and the partials merge on the host). */
+ * mode in which members may share a GPU; without peer mode their partials
+ * then merge on the host). */
 typedef struct kohler_cuda_multi kohler_cuda_multi;
 int kohler_cuda_multi_create(const int *devices, int ndev, kohler_cuda_multi **out);
 void kohler_cuda_multi_destroy(kohler_cuda_multi *group);
@@ -275,8 +278,10 @@ int kohler_cuda_multi_uses_peer(const kohler_cuda_multi *group);
  * kohler::fast_contrast_curve's row-block split, src/fast.cpp:36-62): device
  * b of B owns rows [h*b/B, h*(b+1)/B) (fast.cpp:42,53-55), uploads them plus
  * one halo row and computes the exact band partial (as
- * kohler_cuda_band_curve_device); ONE NCCL all-reduce of the 512 u64
- * partials merges them like merge_accumulators (src/curve.cpp:16-30).
+ * kohler_cuda_band_curve_device); the partials merge like
+ * merge_accumulators (src/curve.cpp:16-30): in peer mode inside the band
+ * kernels' flush (64-bit reductions into the first device's accumulator),
+ * else by ONE NCCL all-reduce of the 512 u64 partial curves.
  * Synchronous; sum/card: 256 u64 host outputs (either may be NULL). */
 int kohler_cuda_multi_curve(kohler_cuda_multi *group, const uint8_t *px, int w, int h,
                             size_t pitch, uint64_t *sum, uint64_t *card);
