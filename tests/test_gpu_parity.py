@@ -218,6 +218,95 @@ def test_selection_device_many_curves(ctx, orc, selection):
         assert out["topk"][i, : int(out["topk_count"][i])].tolist() == tk
 
 
+def _select_patterns(rng, n):
+    """(sums, cards) curves that stress the run / maxima rules: long plateaus
+    across lane boundaries (8 thresholds per lane), alternating values (more
+    than 32 maxima: the ranked top-k over 4 candidates per lane), sparse
+    defined masks, equal maxima (ties to the smaller t), single defined
+    entries, monotone ramps."""
+    sums = np.zeros((n, 256), np.uint64)
+    card = np.ones((n, 256), np.uint64)
+    for i in range(n):
+        kind = i % 8
+        if kind == 0:    # plateaus of random length, few distinct values
+            v = np.repeat(rng.integers(0, 4, 256), rng.integers(1, 40, 256))[:256]
+        elif kind == 1:  # alternating: ~128 maxima, many equal
+            v = (np.arange(256) % 2) * rng.integers(1, 3, 256)
+        elif kind == 2:  # sparse defined mask over a noisy curve
+            v = rng.integers(0, 50, 256)
+            card[i] = (rng.random(256) < 0.15).astype(np.uint64)
+        elif kind == 3:  # equal peaks on a flat floor
+            v = np.zeros(256, np.int64)
+            v[rng.choice(256, rng.integers(1, 20), replace=False)] = 7
+        elif kind == 4:  # one defined entry / one defined run at a lane edge
+            v = rng.integers(1, 9, 256)
+            card[i] = 0
+            a = int(rng.integers(0, 256))
+            card[i, a:a + int(rng.integers(1, 10))] = 1
+        elif kind == 5:  # monotone up, then down (one maximum), plateau top
+            a = int(rng.integers(1, 255))
+            v = np.minimum(np.arange(256), a) - np.maximum(np.arange(256) - a - int(rng.integers(0, 9)), 0)
+            v = v - v.min()
+        elif kind == 6:  # noisy with fractional means (card > 1)
+            v = rng.integers(0, 1000, 256)
+            card[i] = rng.integers(1, 7, 256).astype(np.uint64)
+        else:            # two-valued blocks aligned to the 8-threshold lanes
+            v = np.repeat(rng.integers(0, 3, 32), 8)
+        sums[i] = np.asarray(v, np.int64).astype(np.uint64)
+        sums[i][card[i] == 0] = 0
+    return sums, card
+
+
+@pytest.mark.parametrize("k", [1, 2, 6, 40, 200])
+def test_selection_rule_patterns(ctx, orc, k):
+    """select256_kernel (votes / indexed shuffles / ranked top-k) against the
+    oracle's restatement of threshold.cpp:25-82 on adversarial curve shapes."""
+    rng = np.random.default_rng(1000 + k)
+    n = 640
+    sums, card = _select_patterns(rng, n)
+    ds = torch.from_numpy(sums.view(np.int64)).cuda()
+    dc = torch.from_numpy(card.view(np.int64)).cuda()
+    out = {"values": torch.zeros((n, 256), dtype=torch.float64, device="cuda"),
+           "defined": torch.zeros((n, 256), dtype=torch.uint8, device="cuda"),
+           "t0": torch.zeros(n, dtype=torch.int32, device="cuda"),
+           "topk": torch.full((n, k), -7, dtype=torch.int32, device="cuda"),
+           "topk_count": torch.zeros(n, dtype=torch.int32, device="cuda"),
+           "status": torch.zeros(n, dtype=torch.int32, device="cuda")}
+    ctx.select_device(ds, dc, n, 256, k, out)
+    torch.cuda.synchronize()
+    t0 = out["t0"].cpu().numpy()
+    cnt = out["topk_count"].cpu().numpy()
+    tk = out["topk"].cpu().numpy()
+    st = out["status"].cpu().numpy()
+    for i in range(n):
+        v, d = orc.mean_contrast(sums[i], card[i])
+        est, etk = orc.top_k(v, d, k)
+        assert int(st[i]) == est, i
+        assert int(t0[i]) == orc.optimal_threshold(v, d), i
+        assert tk[i, : int(cnt[i])].tolist() == etk, (i, i % 8)
+
+
+def test_selection_signed_values(ctx, orc):
+    """Host curves with negative values and -0.0 (the selection orders values
+    through an integer key; -0.0 must tie with +0.0 like the IEEE compare)."""
+    rng = np.random.default_rng(5)
+    for i in range(60):
+        v = rng.integers(-3, 4, 256).astype(np.float64) * 0.5
+        if i % 3 == 0:
+            v[v == 0.0] = -0.0 if i % 2 else 0.0
+            v[rng.integers(0, 256, 40)] = -0.0
+        d = rng.random(256) < (0.9 if i % 2 else 0.3)
+        if not d.any():
+            d[17] = True
+        mc = kb.MeanContrastCurve(v, d)
+        dd = d.astype(np.uint8)
+        assert ctx.optimal_threshold(mc) == orc.optimal_threshold(v, dd)
+        for k in (1, 3, 9):
+            est, etk = orc.top_k(v, dd, k)
+            assert est == 0
+            assert ctx.top_k_local_maxima(mc, k).thresholds == etk, (i, k)
+
+
 def test_selection_errors(ctx):
     mc = kb.MeanContrastCurve(np.array([1.0]), np.array([True]))
     with pytest.raises(ValueError):
