@@ -270,8 +270,9 @@ int kohler_cuda_multi_uses_nccl(const kohler_cuda_multi *group);
  * its exact partial straight into one accumulator on the first device
  * (system-scope 64-bit reductions over NVLink / NVSwitch peer memory) and the
  * first device finishes -- no collective.  The default for ndev > 1 when
- * cudaDeviceCanAccessPeer holds for every member; KOHLER_MULTI_NO_PEER=1 in
- * the environment at creation keeps the NCCL all-reduce. */
+ * cudaDeviceCanAccessPeer and native peer atomics (NVLink) hold from every
+ * member to the first; KOHLER_MULTI_NO_PEER=1 in the environment at creation
+ * keeps the NCCL all-reduce. */
 int kohler_cuda_multi_uses_peer(const kohler_cuda_multi *group);
 
 /* fast_contrast_curve of ONE host image over the group (replaces

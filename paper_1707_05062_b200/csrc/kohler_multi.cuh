@@ -340,8 +340,14 @@ int kohler_cuda_multi_create(const int* devices, int ndev, kohler_cuda_multi** o
         for (int i = 1; i < ndev && peer; ++i) {
             if (devs[i] == devs[0])
                 continue;
-            int can = 0;
-            if (cudaDeviceCanAccessPeer(&can, devs[i], devs[0]) != cudaSuccess || !can) {
+            // the flush uses 64-bit reductions on the first device's memory:
+            // the link must carry native atomics (NVLink does, plain PCIe P2P may not)
+            int can = 0, atom = 0;
+            if (cudaDeviceCanAccessPeer(&can, devs[i], devs[0]) != cudaSuccess || !can ||
+                cudaDeviceGetP2PAttribute(&atom, cudaDevP2PAttrNativeAtomicSupported, devs[i], devs[0]) !=
+                    cudaSuccess ||
+                !atom) {
+                (void)cudaGetLastError();
                 peer = false;
                 break;
             }
