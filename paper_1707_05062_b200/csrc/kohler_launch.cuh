@@ -176,7 +176,12 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
         // C3 +0.4 %; the prime positions per walk amortise over more rows)
         for (long long r = 16; r <= kMaxWalkRows; ++r) {
             const long long ch = (band_rows + r - 1) / r;
-            const double waste = (double)(ch * r - band_rows) / band_rows + 0.5 / r;
+            // idle lanes of the image's last 32-walk group count like wasted rows
+            // (C3: 1080 rows x 120 segments -> R = 90 fills 45 groups exactly;
+            // R = 120 leaves 24 of the 34th group's lanes idle, 2.2 %)
+            const long long tasks = ch * nseg, lanes = (tasks + 31) / 32 * 32;
+            const double waste = (double)(ch * r - band_rows) / band_rows + 0.5 / r +
+                                 (double)(lanes - tasks) / (double)tasks;
             if (waste < best - 1e-12) {
                 best = waste;
                 R = r;
