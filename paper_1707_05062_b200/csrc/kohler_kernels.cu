@@ -22,7 +22,10 @@
 //   direct_kernel      : definition-level curve (direct.cpp restated).
 //   hist_kernel / map_kernel : segmentation (classify / quantize).
 //   luma_kernel        : Rec. 601 colour ingest.
-// kohler_multi.cuh (included at the end) holds the multi-GPU device groups.
+// kohler_multi.cuh (included at the end) holds the multi-GPU device groups:
+// row bands of one image over several GPUs whose K1 flushes add into ONE
+// accumulator on the first GPU over peer memory (no collective), or partial
+// curves merged by one NCCL all-reduce; batches sharded by image.
 #include <cuda_runtime.h>
 
 #include <algorithm>
