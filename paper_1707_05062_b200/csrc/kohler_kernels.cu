@@ -46,7 +46,7 @@ using namespace kohler_dev;
 namespace {
 
 #ifndef KOHLER_MAX_WALK_ROWS
-#define KOHLER_MAX_WALK_ROWS 128
+#define KOHLER_MAX_WALK_ROWS 144
 #endif
 constexpr int kMaxWalkRows = KOHLER_MAX_WALK_ROWS;  // longest K1 column walk (rows)
 constexpr int kAccCopiesSingle = 8;  // spread the per-image REDG contention

@@ -172,8 +172,10 @@ int launch_wide(kohler_cuda_ctx* ctx, const uint8_t* px, int n, int w, int band_
     long long R = 64;
     {
         double best = 1e30;
-        // up to 128 rows per walk (measured against 64: C2 +1.3 %, C4 +2.6 %,
-        // C3 +0.4 %; the prime positions per walk amortise over more rows)
+        // up to 144 rows per walk (128 measured against 64: C2 +1.3 %, C4 +2.6 %,
+        // C3 +0.4 %; the prime positions per walk amortise over more rows.  144
+        // lets C2's 3456 rows split into 24 x 144 with 243 full groups and C3's
+        // 1080 into 8 x 135 with 30: C2 +0.3 %, C3 +0.5 % over a cap of 128)
         for (long long r = 16; r <= kMaxWalkRows; ++r) {
             const long long ch = (band_rows + r - 1) / r;
             // idle lanes of the image's last 32-walk group count like wasted rows
