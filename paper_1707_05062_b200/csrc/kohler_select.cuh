@@ -165,6 +165,14 @@ select256_kernel(const SelectParams p)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const uint32_t g = (uint32_t)lane + 32u * i;
+                KCHK({
+                    kohler_walk::chk_sm(buf + 16u * sel256_slot(g), 16);
+                    kohler_walk::chk_sm(buf + 16u * sel256_slot(g + 128u), 16);
+                    kohler_walk::chk_g(gs + 16u * g, 16, reinterpret_cast<const uint8_t*>(p.sums),
+                                       reinterpret_cast<const uint8_t*>(p.sums + (size_t)p.n_curves * 256));
+                    kohler_walk::chk_g(gc + 16u * g, 16, reinterpret_cast<const uint8_t*>(p.cards),
+                                       reinterpret_cast<const uint8_t*>(p.cards + (size_t)p.n_curves * 256));
+                });
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(buf + 16u * sel256_slot(g)),
                              "l"(gs + 16u * g)
                              : "memory");
@@ -187,6 +195,10 @@ select256_kernel(const SelectParams p)
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+                KCHK({
+                    kohler_walk::chk_sm(buf + 16u * sel256_slot(4u * lane + q), 16);
+                    kohler_walk::chk_sm(buf + 16u * sel256_slot(4u * lane + q + 128u), 16);
+                });
                 const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(
                     sbuf_w + 16u * sel256_slot(4u * lane + q));
                 const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(

@@ -394,6 +394,7 @@ __device__ int warp_select256_regs(const double (&v)[8], const bool (&d)[8], int
 #pragma unroll
     for (int j = 0; j < 8; ++j)
         if (maxmask & (1u << j)) {
+            KCHK(if (pos < 0 || pos >= 128) chk_fail(4, (uint32_t)pos));  // <= 128 maxima exist
             mk[pos] = order_key(v[j]);
             mt[pos] = 8 * lane + j;
             ++pos;
