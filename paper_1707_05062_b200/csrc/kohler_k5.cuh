@@ -404,39 +404,45 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 return __shfl_sync(0xFFFFFFFFu, x, 24 + gi);  // the image's (= warp's) total
             };
             const long long tc = quad_scan(cd);
-            const long long tg = quad_scan(h2);  // h2 -> g (sum first difference)
+            const long long tg = quad_scan(h2);   // h2 -> g, local to the warp's 16 keys
+            const long long tsl = quad_scan(h2);  // g -> sum, local too (earlier warps enter below)
             if (q4 == 0) {
                 tot[(0 * 16 + warp) * NG + gi] = tc;
                 tot[(1 * 16 + warp) * NG + gi] = tg;
+                tot[(2 * 16 + warp) * NG + gi] = tsl;
             }
             __syncthreads();
-            // carry of the earlier warps' totals: the image's 4 lanes (q4)
-            // load 4 warps' totals each, independent loads, then two
-            // shuffles (a serial 15-load chain made warp 15 the round's
-            // straggler at the final barrier)
-            auto carry = [&](int kind) -> long long {
-                long long c = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int w2 = 4 * q4 + i;
-                    if (w2 < warp)
-                        c += tot[(kind * 16 + w2) * NG + gi];
-                }
-                c += __shfl_xor_sync(0xFFFFFFFFu, c, 8);
-                c += __shfl_xor_sync(0xFFFFFFFFu, c, 16);
-                return c;
-            };
-            const long long cc = carry(0), cg = carry(1);
+            // The earlier warps' part, from their totals alone (one exchange, no
+            // third barrier): with cg = sum of earlier tg, key k of the warp has
+            //   g[k]   = g_local[k] + cg
+            //   sum[k] = sum_local[k] + (k + 1) cg + cs,
+            //   cs     = sum over earlier warps w' of (tsl(w') + 16 cg(w'))
+            //          = sum over w' < w of (tsl(w') + 16 (w - 1 - w') tg(w')).
+            // The image's 4 lanes (q4) load 4 warps' totals each, independent
+            // loads, then two shuffles (a serial 15-load chain made warp 15
+            // the round's straggler at the final barrier).
+            long long cc = 0, cg = 0, cs = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                cd[i] += cc;  // card
-                h2[i] += cg;  // g
+                const int w2 = 4 * q4 + i;
+                if (w2 < warp) {
+                    const long long g2 = tot[(1 * 16 + w2) * NG + gi];
+                    cc += tot[(0 * 16 + w2) * NG + gi];
+                    cg += g2;
+                    cs += tot[(2 * 16 + w2) * NG + gi] + 16ll * (long long)(warp - 1 - w2) * g2;
+                }
             }
-            const long long ts = quad_scan(h2);  // g -> sum, without the carry of earlier warps' g
-            if (q4 == 0)
-                tot[(2 * 16 + warp) * NG + gi] = ts;
-            __syncthreads();
-            const long long cs = carry(2);
+            cc += __shfl_xor_sync(0xFFFFFFFFu, cc, 8);
+            cg += __shfl_xor_sync(0xFFFFFFFFu, cg, 8);
+            cs += __shfl_xor_sync(0xFFFFFFFFu, cs, 8);
+            cc += __shfl_xor_sync(0xFFFFFFFFu, cc, 16);
+            cg += __shfl_xor_sync(0xFFFFFFFFu, cg, 16);
+            cs += __shfl_xor_sync(0xFFFFFFFFu, cs, 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cd[i] += cc;                                      // card
+                h2[i] += (long long)(4 * q4 + i + 1) * cg + cs;  // sum
+            }
             const long long im = i0 + gi;
             if (im < p.n) {
                 // 64-bit stores straight from the register pairs: STG.128 made
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     oc[i] = (uint64_t)cd[i];
-                    os[i] = (uint64_t)(h2[i] + cs);
+                    os[i] = (uint64_t)h2[i];
                 }
                 if (p.hist_out) {
 #pragma unroll
