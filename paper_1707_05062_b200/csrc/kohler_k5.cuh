@@ -68,10 +68,7 @@ struct TwLayout {
     static constexpr uint32_t kRingBytes = kTwWarps * kSlots * kSlot + 128;
     static constexpr uint32_t kCorr = kRingBytes;  // int[NG][260] (not with one W copy)
     static constexpr uint32_t kTot = kCorr + (kOneW ? 0u : NG * kTwCorrStride);  // i64 [3][16 warps][NG] scan carries
-    // LG = 4 flush: boundary values handed from warp w - 1 to warp w
-    static constexpr uint32_t kXch = kTot + 3 * 16 * NG * 8;  // uint4 [16 warps][8 images]
-    static constexpr uint32_t kXchC = kXch + 16 * 8 * 16;     // int [16 warps][8 images]
-    static constexpr uint32_t kEnd = kXchC + 16 * 8 * 4;
+    static constexpr uint32_t kEnd = kTot + 3 * 16 * NG * 8;
     static_assert(kEnd + 1024 <= kHistAbs, "K5 scratch under the counter block");
 };
 
@@ -311,15 +308,15 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
             // Cooperative flush for 8 images per round (C5): warp w owns the
             // keys [16 w, 16 w + 16) of all 8 images; lane L takes image
             // gi = L & 7, keys t0 .. t0 + 3 (t0 = 16 w + 4 (L >> 3)) of the W
-            // table and rows 2 t0 .. 2 t0 + 7 of the Hs table.  A group's 4
+            // table and rows 2 t0 - 1 .. 2 t0 + 6 of the Hs table.  A group's 4
             // lane words of a counter row are one 16-byte piece and the 8
             // lanes of a quarter warp (one LDS.128 wavefront) take 8 images,
             // i.e. 8 bank quads: conflict free.  Every piece has exactly one
             // reader, which clears it right after reading (no second pass).
-            // The reconstruction of keys t0.. also needs the last key / the
-            // last three Hs rows of the previous owner: a shuffle from lane
-            // L - 8, or for the first quarter warp from warp w - 1 through
-            // shared memory.
+            // No lane needs another lane's counters: the terms a lane holds
+            // for the NEXT lane's first key travel with its scan total (see
+            // dA below), so the flush has one barrier -- the exchange of the
+            // warps' scan totals.
             const int gi = lane & 7, q4 = lane >> 3;
             const int t0 = 16 * warp + 4 * q4;
             uint32_t hh[4], bb[4];  // hist(t0 + i), B sums
@@ -331,14 +328,21 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 hh[i] = (v.x & 0xFFFFu) + (v.y & 0xFFFFu) + (v.z & 0xFFFFu) + (v.w & 0xFFFFu);
                 bb[i] = (v.x >> 16) + (v.y >> 16) + (v.z >> 16) + (v.w >> 16);
             }
-            uint32_t hs[8];  // Hs rows 2 t0 + i (row 511 is the dummy row: cleared, not counted)
+            // Hs rows 2 t0 - 1 + i: the eight rows whose terms all fall on this
+            // lane's keys t0 .. t0 + 3 or -- the last two -- on key t0 + 4 (below).
+            // Row -1 does not exist; row 511 (the dummy row of neutralised
+            // events) is never read, so it needs no clearing either.
+            uint32_t hs[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int r = 2 * t0 + i;
-                uint4* c = reinterpret_cast<uint4*>(hist + r * 256 + gi * 16);
-                const uint4 v = *c;
-                *c = make_uint4(0, 0, 0, 0);
-                hs[i] = r < 511 ? v.x + v.y + v.z + v.w : 0u;
+                const int r = 2 * t0 - 1 + i;
+                hs[i] = 0u;
+                if (r >= 0) {
+                    uint4* c = reinterpret_cast<uint4*>(hist + r * 256 + gi * 16);
+                    const uint4 v = *c;
+                    *c = make_uint4(0, 0, 0, 0);
+                    hs[i] = v.x + v.y + v.z + v.w;
+                }
             }
             int crv[4];  // corr(t0 + i): the lane-striped second W copy
 #pragma unroll
@@ -348,64 +352,47 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 *c = make_uint4(0, 0, 0, 0);
                 crv[i] = (int)(v.x + v.y + v.z + v.w);
             }
-            // previous owner's hist(t0 - 1), Hs rows 2 t0 - 3 .. 2 t0 - 1, corr(t0 - 1)
-            uint32_t ph = __shfl_up_sync(0xFFFFFFFFu, hh[3], 8);
-            uint32_t pa = __shfl_up_sync(0xFFFFFFFFu, hs[5], 8);
-            uint32_t pb = __shfl_up_sync(0xFFFFFFFFu, hs[6], 8);
-            uint32_t pc = __shfl_up_sync(0xFFFFFFFFu, hs[7], 8);
-            int pcr = __shfl_up_sync(0xFFFFFFFFu, crv[3], 8);
-            uint4* xch = reinterpret_cast<uint4*>(sm + Lay::kXch);
-            int* xchc = reinterpret_cast<int*>(sm + Lay::kXchC);
-            if (q4 == 3) {
-                xch[warp * 8 + gi] = make_uint4(hh[3], hs[5], hs[6], hs[7]);
-                xchc[warp * 8 + gi] = crv[3];
-            }
-            __syncthreads();
-            if (q4 == 0) {
-                if (warp > 0) {
-                    const uint4 x = xch[(warp - 1) * 8 + gi];
-                    ph = x.x;
-                    pa = x.y;
-                    pb = x.z;
-                    pc = x.w;
-                    pcr = xchc[(warp - 1) * 8 + gi];
-                } else {
-                    ph = pa = pb = pc = 0u;
-                    pcr = 0;
-                }
-            }
+            // h2(u) = 4 hist(u-1) - corr(u-1) - Hs(2u-3) - 2 Hs(2u-2) - Hs(2u-1).
+            // With the rows above a lane holds every term of h2(t0+1 .. t0+3),
+            // the Hs(2 t0 - 1) term of h2(t0), and all other terms of the NEXT
+            // lane's first key, h2(t0+4) -- its "deferred" part dA.  Everything
+            // downstream is a prefix scan, and a term of key t0 + 4 acts on
+            // exactly the keys of the later lanes: dA joins this lane's scan
+            // TOTAL but not its own elements, and no lane needs another lane's
+            // counters (no hand-off, no barrier before the scans).
             long long cd[4], h2[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
                 cd[i] = (long long)bb[i] - 4ll * (long long)hh[i];
-            // h2(u) = 4 hist(u-1) - corr(u-1) - hs(2u-3) - 2 hs(2u-2) - hs(2u-1), u = t0 + i
-            h2[0] = t0 == 0 ? 0
-                            : 4ll * ph - (long long)pcr - (long long)pa - 2ll * pb - (long long)pc;
-            h2[1] = 4ll * hh[0] - (long long)crv[0] - (long long)pc - 2ll * hs[0] - (long long)hs[1];
-            h2[2] = 4ll * hh[1] - (long long)crv[1] - (long long)hs[1] - 2ll * hs[2] - (long long)hs[3];
-            h2[3] = 4ll * hh[2] - (long long)crv[2] - (long long)hs[3] - 2ll * hs[4] - (long long)hs[5];
-            // scans: lane-local, then across the image's 4 lanes (a quad)
+            h2[0] = -(long long)hs[0];
+            h2[1] = 4ll * hh[0] - (long long)crv[0] - (long long)hs[0] - 2ll * hs[1] - (long long)hs[2];
+            h2[2] = 4ll * hh[1] - (long long)crv[1] - (long long)hs[2] - 2ll * hs[3] - (long long)hs[4];
+            h2[3] = 4ll * hh[2] - (long long)crv[2] - (long long)hs[4] - 2ll * hs[5] - (long long)hs[6];
+            const long long dA = 4ll * hh[3] - (long long)crv[3] - (long long)hs[6] - 2ll * hs[7];
+            // scans: lane-local, then across the image's 4 lanes (a quad);
+            // `extra` counts in the lane's total only
             long long* tot = reinterpret_cast<long long*>(sm + Lay::kTot);  // [3][16][NG]
-            auto quad_scan = [&](long long (&v)[4]) -> long long {
+            auto quad_scan = [&](long long (&v)[4], long long extra) -> long long {
 #pragma unroll
                 for (int i = 1; i < 4; ++i)
                     v[i] += v[i - 1];
-                long long x = v[3];  // the image's 4 lanes are gi, gi + 8, gi + 16, gi + 24
+                const long long own = v[3] + extra;
+                long long x = own;  // the image's 4 lanes are gi, gi + 8, gi + 16, gi + 24
 #pragma unroll
                 for (int off = 1; off < 4; off <<= 1) {
                     const long long y = __shfl_up_sync(0xFFFFFFFFu, x, 8 * off);
                     if (q4 >= off)
                         x += y;
                 }
-                const long long ex = x - v[3];
+                const long long ex = x - own;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
                     v[i] += ex;
                 return __shfl_sync(0xFFFFFFFFu, x, 24 + gi);  // the image's (= warp's) total
             };
-            const long long tc = quad_scan(cd);
-            const long long tg = quad_scan(h2);   // h2 -> g, local to the warp's 16 keys
-            const long long tsl = quad_scan(h2);  // g -> sum, local too (earlier warps enter below)
+            const long long tc = quad_scan(cd, 0);
+            const long long tg = quad_scan(h2, dA);  // h2 -> g, local to the warp's 16 keys
+            const long long tsl = quad_scan(h2, 0);  // g -> sum, local too (earlier warps enter below)
             if (q4 == 0) {
                 tot[(0 * 16 + warp) * NG + gi] = tc;
                 tot[(1 * 16 + warp) * NG + gi] = tg;
@@ -560,10 +547,10 @@ __global__ void __launch_bounds__(kTwThreads, 1) twalk_kernel(const TwParams p)
                 reinterpret_cast<int*>(sm + Lay::kCorr)[i] = 0;
         }
         // LG = 4 needs no barrier here: every counter piece was cleared before
-        // the hand-off barrier, and the next round touches the exchange /
-        // carry arrays only after its own barriers, which every warp reaches
-        // after this round's last read of them; a warp done with its stores
-        // starts the next round's walk while the others finish theirs
+        // the totals barrier, and the next round writes the totals only behind
+        // its walk-end barrier, which every warp reaches after this round's
+        // last read of them; a warp done with its stores starts the next
+        // round's walk while the others finish theirs
         if constexpr (LG != 4)
             __syncthreads();
         TWCYC(4);
