@@ -1,10 +1,14 @@
 """The multi-GPU C ABI (kohler_cuda_multi_*, include/kohler_cuda.h "device
-groups"): one host thread, one context + one NCCL communicator per device.
-Only one GPU is visible to the tests, so the group has one member here; the
-row-band split and the merge run through the same code for any size (the
-band partials of every split are checked in test_gpu_parity.py and the
-N > 1 host logic in test_bands_gloo.py).  Results must equal the oracle's
-bit for bit (reference fast.cpp:36-62 for any split)."""
+groups"): one host thread, one context per device.  Only one GPU is visible
+to the tests: a group of that one device runs the NCCL all-reduce path
+(world 1), and KOHLER_MULTI_VIRTUAL=1 groups of 3-8 members on the same GPU
+run the B-way row-block split in both merge forms -- peer mode (the members'
+band kernels add straight into the first member's accumulator, one
+finish_kernel behind their events) and per-member partial curves merged on
+the host (the stand-in for the all-reduce).  The band partials of every split
+are also checked in test_gpu_parity.py and the N > 1 host logic in
+test_bands_gloo.py.  Results must equal the oracle's bit for bit (reference
+fast.cpp:36-62 for any split)."""
 import numpy as np
 import pytest
 
