@@ -860,7 +860,8 @@ def measure_e2e(ctx, img, args, dev_index):
     placed on the GPU's NUMA node while the pinned buffer is allocated and
     the calls run (pinned pages first-touched there), and the box's raw
     pinned H2D copy rate is recorded beside it (the floor of this path).
-    Wall clock, best of three blocks of n steps each."""
+    Wall clock, best of five blocks of n steps each (a box's pinned H2D rate
+    has slow stretches of tens of milliseconds, profiles/r02e)."""
     import ctypes as C
     h, w = img.shape
     old_aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
@@ -918,7 +919,7 @@ def measure_e2e(ctx, img, args, dev_index):
         def best(block):
             block()  # warm-up block
             el = []
-            for _ in range(3):
+            for _ in range(5):
                 st = time.perf_counter()
                 block()
                 el.append(time.perf_counter() - st)
@@ -950,7 +951,7 @@ def measure_e2e(ctx, img, args, dev_index):
             "box_pinned_h2d_gbs": h2d_gbs,
             "host_placement": placed or "unpinned (NUMA node of the GPU unknown)",
             "path": "kohler_cuda_submit / kohler_cuda_collect (host C ABI, two steps in flight), "
-                    "pinned input, wall clock, best of 3 blocks; sync_* = kohler_cuda_analyze"}
+                    "pinned input, wall clock, best of 5 blocks; sync_* = kohler_cuda_analyze"}
 
 
 if __name__ == "__main__":
